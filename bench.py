@@ -1,0 +1,348 @@
+"""FFT-PIM potential-evaluation benchmark (BASELINE.json metric: source=observer
+points/sec per evaluation, HBM-roofline fraction, relative L2 error).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+A step is one SolvePlan.evaluate (solver.py:24-25) of the config's charge
+vector, inputs resident in HBM.  Default workload: configs[1] = C2 (1D-periodic
+Helmholtz, N = 65,536, 64^3 grid, order 3) -- the BASELINE config that fits
+one GPU and that the reference itself can run.  C1/C2/C3 shard as replicas
+(SURVEY.md 8e): under torchrun each rank evaluates its own replica, value =
+total points of all ranks / max-over-ranks time ("scaling": "weak").
+
+`--impl reference` times the reference algorithm on the host CPU (the numpy
+oracle port; the reference is pure Python/numpy): plan built once by the
+oracle (multi-process), then single-threaded numpy evaluations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_2312_02376_b200.workloads import CONFIGS, make_inputs  # noqa: E402
+
+METRIC = "source=observer points/sec per FFT-PIM potential eval"
+UNIT = "points/s"
+HBM_FALLBACK = 6650.0
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def problem_objects(fp, c):
+    w = CONFIGS[c]
+    pos, q = make_inputs(c)
+    if w.excitations > 1:
+        raise SystemExit("C5 (batched excitations) is not wired into bench.py yet")
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=w.kshift,
+                               regime=fp.Regime(w.regime))
+    return w, pos, q, cfg, fp.TargetBox(w.D), fp.SolverParams(**w.params())
+
+
+def stage_bytes(w, info, n_far):
+    """Algorithmic bytes per evaluation stage.
+    q, u and grid values are complex128 (16 B); coefficients 8 B (NPSP) or 16 B."""
+    N = M = w.n_points
+    ng = int(np.prod(info.near_dims))
+    nfft = int(np.prod(info.fft_dims))
+    P = int(info.n_pairs)
+    sc = 8 if info.real_coefficients else 16
+    return {
+        "permute_q": 16 * N + 4 * N + 16 * N,
+        "far_project": N * (24 + 16) + 16 * n_far,
+        "near_project": N * (24 + 16) + 16 * nfft,       # padded grid written once (zeros included)
+        "fft_forward": 2 * 16 * nfft,
+        "spectrum_mul": 3 * 16 * nfft,
+        "fft_inverse": 2 * 16 * nfft,
+        "observers": M * 24 + 16 * ng + P * (sc + 4) + 8 * M + 16 * N + 16 * M,
+    }
+
+
+def cpu_baseline_from_plan(w, plan, pos, q, budget_s=20.0):
+    """Time the oracle's evaluation (the reference algorithm: eval_near + eval_far,
+    nearzone.py:490-525 + farzone.py:150-159) on this host's CPU with the plan
+    operands exported from the GPU plan (identical pair lists -- tests pin that)."""
+    from oracle import far_engine as fe
+    from oracle import near_engine as ne
+    from oracle.lagrange import far_grids, make_stencil, near_grid
+    from oracle.problem import make_problem
+    pb = make_problem(w.dim, L=w.L, D=w.D, k0=w.k0, kshift=w.kshift, regime=w.regime, **w.params())
+    nat = plan.native
+    dims = tuple(int(v) for v in nat.info.near_dims)
+    grid = near_grid(pb.D, dims)
+    margin = tuple(1e-9 * max(grid.spacing[a], 1.0) for a in range(3))
+    st = make_stencil(grid, pos, pb.near_order, margin)
+    p_obs = plan.near.pair_obs
+    cnt = np.bincount(p_obs, minlength=len(pos))
+    seg_obs = np.nonzero(cnt)[0]
+    seg_starts = (np.cumsum(cnt) - cnt)[seg_obs]
+    near = ne.NearPlan(pb, grid, st, st, None, plan.near.kernel_hat, None, None, None, p_obs,
+                       plan.near.pair_src, plan.near.pair_code, plan.near.pair_coef, seg_obs, seg_starts, 0, 0, 0)
+    fdims = tuple(pb.far_grid[a] if pb.D[a] > 0.0 else 1 for a in range(3))
+    sg, og = far_grids(pb.D, fdims)
+    fm = tuple(sg.spacing[a] if sg.dims[a] > 1 else 0.0 for a in range(3))
+    far = fe.FarPlan(pb, sg, og, make_stencil(sg, pos, pb.far_order, fm), make_stencil(og, pos, pb.far_order, fm),
+                     plan.far.kernel, plan.far.kernel_terms)
+    times, u = [], None
+    t_start = time.perf_counter()
+    while len(times) < 5 and (len(times) < 2 or time.perf_counter() - t_start < budget_s):
+        t0 = time.perf_counter()
+        u = ne.eval_near(near, q) + fe.eval_far(far, q)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": w.n_points / best, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(times)} full {w.name} evaluations (N={w.n_points}) of the numpy oracle "
+                      f"(reference algorithm, single-threaded numpy eval loops; host nproc={os.cpu_count()}), "
+                      f"plan operands exported from the GPU plan; best of {len(times)} (cli.py:360-366)",
+            "seconds_per_eval": best}, u
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2312_02376_b200 as fp
+    from paper_2312_02376_b200 import _native as nat
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, pos, q, cfg, box, prm = problem_objects(fp, args.config)
+    t0 = time.perf_counter()
+    plan = fp.build_plan(cfg, box, fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos), prm, device=local)
+    build_s = time.perf_counter() - t0
+    info = plan.native.info
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    q_dev = torch.from_numpy(q).to(f"cuda:{local}")
+    u_dev = torch.empty(w.n_points, dtype=torch.complex128, device=f"cuda:{local}")
+    nplan = plan.native
+
+    def step():
+        nplan.evaluate_into(q_dev.data_ptr(), u_dev.data_ptr(), 1, nat.ALL, sptr)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = nat.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = (nat.launch_count() - launches0) // args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * w.n_points / (ms_max * 1e-3)
+
+    # per-stage device times (events between stages, same stream), averaged
+    prof = {k: 0.0 for k in nat.STAGES}
+    reps = 10
+    for _ in range(reps):
+        for k, v in nplan.profile(q_dev.data_ptr(), u_dev.data_ptr(), nat.ALL, sptr).items():
+            prof[k] += v / reps
+    nbytes = stage_bytes(w, info, int(np.prod(info.far_dims)))
+    own = {k: v for k, v in prof.items() if not k.startswith("fft_")}
+    dom = max(own, key=own.get)
+    peak, peak_kind = measured_peak()
+    achieved = nbytes[dom] / (prof[dom] * 1e-3) / 1e9
+    traffic = None
+    summ = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(summ):
+        try:
+            traffic = json.load(open(summ)).get(f"C{args.config}", {}).get(dom)
+        except Exception:  # noqa: BLE001
+            traffic = None
+
+    # end to end through the public API with host buffers (pinned), H2D + D2H inside
+    q_pin = torch.from_numpy(q).pin_memory()
+    u_pin = torch.empty(w.n_points, dtype=torch.complex128).pin_memory()
+    q_host, u_host = q_pin.numpy(), u_pin.numpy()
+    for _ in range(2):
+        plan.native.evaluate(q_host, out=u_host)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        plan.native.evaluate(q_host, out=u_host)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * w.n_points / float(te.item())
+
+    # parity of this very run against the reference's own output (C1/C2 fixtures)
+    rel = None
+    gpath = os.path.join(REPO, "tests", "golden", f"c{args.config}_full.npz")
+    if os.path.exists(gpath):
+        ref = np.load(gpath)["u"]
+        got = u_dev.cpu().numpy()
+        rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, u_cpu = cpu_baseline_from_plan(w, plan, pos, q)
+        if rel is None:
+            rel = float(np.linalg.norm(u_dev.cpu().numpy() - u_cpu) / np.linalg.norm(u_cpu))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "complex128/f64", "data": "synthetic (seeded, workloads.py)",
+            "config": {"workload": w.name, "N": w.n_points, "near_grid": list(w.near_grid),
+                       "near_order": w.near_order, "regime": w.regime, "pairs": int(info.n_pairs),
+                       "parallelism": f"replicas x{world}",
+                       "l2": "working set > L2 (correction stream alone "
+                             f"{int(info.n_pairs) * (12 if info.real_coefficients else 20) / 1e6:.0f} MB)"},
+            "rel_l2_vs_reference": rel,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                         "algorithmic_bytes": nbytes[dom], "kernel_ms": prof[dom]},
+            "stages_ms": prof,
+            "stage_gbs": {k: nbytes[k] / (prof[k] * 1e-3) / 1e9 for k in nbytes if prof.get(k, 0) > 0},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * w.n_points,
+                    "d2h_bytes_per_step": 16 * w.n_points},
+            "gpu_launches": int(launches),
+            "build_seconds": build_s,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference algorithm on the host CPU (numpy oracle port; the reference itself
+    is Python and is not shipped to the GPU box)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.parallel import build_plan_parallel
+    from oracle.problem import make_problem
+    w = CONFIGS[args.config]
+    pos, q = make_inputs(args.config)
+    pb = make_problem(w.dim, L=w.L, D=w.D, k0=w.k0, kshift=w.kshift, regime=w.regime, **w.params())
+    t0 = time.perf_counter()
+    plan = build_plan_parallel(pb, pos)
+    build_s = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        plan.evaluate(q)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        plan.evaluate(q)
+        times.append(time.perf_counter() - t0)
+    sec = float(np.median(times))
+    value = w.n_points / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "complex128/f64",
+        "data": "synthetic (seeded, workloads.py)",
+        "config": {"workload": w.name, "N": w.n_points, "near_grid": list(w.near_grid),
+                   "near_order": w.near_order, "regime": w.regime, "pairs": int(plan.near.pair_obs.size)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"each step = one full {w.name} evaluation by the numpy oracle "
+                                   f"(reference algorithm; its eval loops are single-threaded numpy); plan "
+                                   f"built once by the oracle over {os.cpu_count()} processes in {build_s:.1f} s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build_seconds": build_s,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

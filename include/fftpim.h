@@ -1,0 +1,152 @@
+/*
+ * fftpim.h -- C ABI of the B200-native FFT-PIM potential evaluation.
+ *
+ * Drop-in boundary for the reference's hot path (perisum 0.1.0, Python):
+ *   build_plan(cfg, box, src, obs, params)   /root/reference/pkg/src/perisum/solver.py:35-45
+ *   SolvePlan.evaluate(q) = eval_near+eval_far /root/reference/pkg/src/perisum/solver.py:24-25
+ *   build_near_plan / eval_near               /root/reference/pkg/src/perisum/nearzone.py:194, 490
+ *   build_far_plan / eval_far                 /root/reference/pkg/src/perisum/farzone.py:76, 150
+ * Plain C types only: no torch, no CUDA types in the signatures (streams are
+ * passed as void* = cudaStream_t).  All arithmetic is fp64 / complex128;
+ * complex arrays are interleaved (re, im) doubles, exactly numpy complex128.
+ *
+ * Status codes map 1:1 onto the reference's exception classes
+ * (/root/reference/pkg/src/perisum/errors.py:4-37):
+ */
+#ifndef FFTPIM_H
+#define FFTPIM_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FFTPIM_API __attribute__((visibility("default")))
+#else
+#define FFTPIM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum FftpimStatus {
+    FFTPIM_OK = 0,
+    FFTPIM_VALIDATION = 1,      /* ValidationError      model.py:211-297            */
+    FFTPIM_DOMAIN = 2,          /* DomainError          nearzone.py:410-416, pgf.py:143-147 */
+    FFTPIM_WOOD_ANOMALY = 3,    /* WoodAnomalyError     pgf.py:239-240, 257-261, 271-275 */
+    FFTPIM_NOT_CONVERGED = 4,   /* NotConvergedError    farzone.py:115-119, pgf.py:268-270 */
+    FFTPIM_SEPARATION = 5,      /* SeparationError      pgf.py:227-229, 343-344     */
+    FFTPIM_KERNEL_CACHE = 6,    /* KernelCacheError     farzone.py:186-212          */
+    FFTPIM_CUDA = 7,            /* CUDA / cuFFT failure (no reference counterpart)  */
+    FFTPIM_VALUE = 8            /* ValueError (length mismatch, bad grid)  nearzone.py:495-496 */
+};
+
+/* Regime codes follow the PIMF blob codes, farzone.py:29. */
+enum FftpimRegime { FFTPIM_DYNAMIC = 1, FFTPIM_STATIC_SHIFTED = 2, FFTPIM_NPSP = 3 };
+
+/* Evaluation parts: eval_near (nearzone.py:490) and eval_far (farzone.py:150). */
+enum FftpimParts { FFTPIM_NEAR = 1, FFTPIM_FAR = 2, FFTPIM_ALL = 3 };
+
+/* PeriodicityConfig (model.py:42-76) + TargetBox (model.py:80-88) +
+ * SolverParams (model.py:166-190) + the point sets (model.py:99-126). */
+typedef struct FftpimProblem {
+    int32_t dim;                /* number of periodic axes: 1 (x), 2 (x,y), 3 (x,y,z) */
+    int32_t regime;             /* FftpimRegime */
+    double L[3];                /* lattice periods */
+    double D[3];                /* target box extent */
+    double k0[2];               /* complex wavenumber (re, im) */
+    double kshift[3][2];        /* complex phase shift per axis */
+    int32_t i_d;                /* near-image half width */
+    int32_t near_order;
+    int32_t near_grid[3];       /* resolved near grid; {0,0,0} = auto (model.py:146-162) */
+    int32_t far_order;
+    int32_t far_grid[3];
+    double series_tol;
+    int32_t er_range_boxes;
+    int64_t n_src;
+    int64_t n_obs;
+    const double* src_pos;      /* (n_src, 3) row-major, HOST memory */
+    const double* obs_pos;      /* (n_obs, 3) row-major, HOST memory; NULL = same as src */
+    int32_t same_points;        /* 1: observers are the sources (nearzone.py:241-243) */
+    int32_t device;             /* CUDA device ordinal */
+} FftpimProblem;
+
+/* Summary read by the reference CLI (cli.py:232-236) and by the tests. */
+typedef struct FftpimInfo {
+    int32_t near_dims[3];
+    int32_t fft_dims[3];        /* doubled (circulant) dims */
+    int32_t far_dims[3];
+    int32_t join_radius[3];
+    int32_t jr_full;
+    int32_t on_axis_offset;     /* 1 when the far source grid was moved off the axis (farzone.py:89-98) */
+    int64_t n_src;
+    int64_t n_obs;
+    int64_t n_pairs;
+    int64_t n_self_pairs;
+    int64_t n_wrapped_pairs;
+    int64_t coincident_kernel_terms;
+    int64_t kernel_terms;       /* worst far-series length */
+    int64_t device_bytes;       /* plan-owned device memory */
+    double build_seconds;
+    int32_t real_coefficients;  /* 1: correction coefficients stored as fp64 (NPSP) */
+} FftpimInfo;
+
+typedef struct FftpimPlan FftpimPlan;
+
+/* Build a plan on `p->device`.  Replaces build_plan (solver.py:35-45), i.e.
+ * build_near_plan (nearzone.py:194-273) + build_far_plan (farzone.py:76-131).
+ * Validation (model.py:211-297) is the caller's job; geometry-dependent errors
+ * (DomainError, WoodAnomaly, NotConverged, Separation) are returned here. */
+FFTPIM_API int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out);
+
+/* u = eval_near + eval_far for `batch` charge vectors.  q: (batch, n_src)
+ * complex128 and u: (batch, n_obs) complex128, both DEVICE pointers, stream
+ * ordered on `stream` (cudaStream_t; NULL = legacy default).  Replaces
+ * SolvePlan.evaluate (solver.py:24-25); parts selects eval_near / eval_far. */
+FFTPIM_API int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch,
+                         int32_t parts, void* stream);
+
+/* Same with HOST q/u (pinned or pageable): H2D copy, evaluate, D2H copy,
+ * synchronous.  This is the call the reference's FFI binding makes. */
+FFTPIM_API int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch,
+                              int32_t parts);
+
+FFTPIM_API int fftpim_plan_info(const FftpimPlan* plan, FftpimInfo* info);
+
+/* Operand export for parity tests (host destination, `bytes` capacity).
+ * Pairs come out in the reference order (nearzone.py:465-478): sorted by
+ * observer index, within an observer in discovery order; indices are the
+ * caller's original point indices. */
+enum FftpimOperand {
+    FFTPIM_PAIR_OBS = 1,        /* int32 (P)            NearZonePlan.pair_obs  */
+    FFTPIM_PAIR_SRC = 2,        /* int32 (P)            NearZonePlan.pair_src  */
+    FFTPIM_PAIR_CODE = 3,       /* int8  (P,3)          NearZonePlan.pair_code */
+    FFTPIM_PAIR_COEF = 4,       /* complex128 (P)       NearZonePlan.pair_coef */
+    FFTPIM_FAR_KERNEL = 5,      /* complex128 (2n-1)^3  FarZonePlan.kernel     */
+    FFTPIM_KERNEL_HAT = 6       /* complex128 fft_dims  NearZonePlan.kernel_hat (numpy scaling) */
+};
+FFTPIM_API int fftpim_plan_export(const FftpimPlan* plan, int32_t which, void* dst, int64_t bytes);
+
+/* Replace the far kernel table (PIMF blob import, farzone.py:103-112). */
+FFTPIM_API int fftpim_plan_set_far_kernel(FftpimPlan* plan, const double* kernel, int64_t n_entries);
+
+FFTPIM_API void fftpim_plan_destroy(FftpimPlan* plan);
+
+/* Thread-local message of the last non-OK status. */
+FFTPIM_API const char* fftpim_last_error(void);
+
+/* One evaluation (batch 1, device pointers) with CUDA events recorded on
+ * `stream` between the stages; stage_ms[0..7] receives the device time of
+ *   0 permute q  1 far projection  2 far grid sum  3 near projection
+ *   4 forward FFT  5 spectrum multiply  6 inverse FFT  7 observer pass
+ * (interpolation + precorrection + far interpolation).  Diagnostic only. */
+#define FFTPIM_N_STAGES 8
+FFTPIM_API int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t parts,
+                                   void* stream, double* stage_ms);
+
+/* Number of kernel launches this library issued since load (evidence counter). */
+FFTPIM_API int64_t fftpim_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTPIM_H */

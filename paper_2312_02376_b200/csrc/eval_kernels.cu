@@ -1,0 +1,270 @@
+// eval_kernels.cu -- the hot path, SolvePlan.evaluate (solver.py:24-25):
+//   K0  q -> sorted order
+//   K1  near projection, owner-computes gather per grid node (grids.py:167-181)
+//   K2  spectrum multiply between the cuFFT passes (nearzone.py:500-504)
+//   K5a far projection, per-warp private grids in shared memory (farzone.py:156)
+//   K5b far grid superposition sum (farzone.py:157-158)
+//   K3+K4+K5c fused observer pass: near interpolation, correction matvec and far
+//       interpolation in one warp per observer (grids.py:183-188, nearzone.py:506-524,
+//       farzone.py:159)
+// Every reduction has a fixed order: results are bitwise reproducible run to run.
+#include "geom.cuh"
+#include "kernels.h"
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+__device__ __forceinline__ cplx warp_sum(cplx v) {
+    for (int o = 16; o > 0; o >>= 1) {
+        v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
+        v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------- K0
+__global__ void k_permute_q(const cplx* __restrict__ q, const int* __restrict__ perm, int64_t n,
+                            cplx* __restrict__ qs) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) qs[i] = q[perm[i]];
+}
+void launch_permute_q(const EvalArgs& a, cudaStream_t s) {
+    if (a.N == 0) return;
+    k_permute_q<<<nblk(a.N, 256), 256, 0, s>>>(a.q, a.src_perm, a.N, a.q_sorted);
+    fftpim_count_launch();
+}
+
+// ---------------------------------------------------------------- K1
+// One thread per element of the zero-padded (2n)^3 buffer: padding slots write
+// 0, grid nodes gather the points whose stencil covers them.  Points are
+// sorted by stencil start, so for fixed (x, y) start offsets the candidate z
+// starts form one contiguous CSR range.
+template <int W>
+__global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= a.n_fft) return;
+    const int c1 = a.cdims[1], c2 = a.cdims[2];
+    const int z = (int)(t % c2), y = (int)((t / c2) % c1), x = (int)(t / ((int64_t)c1 * c2));
+    const StencilGeom& g = a.g;
+    cplx acc = mk(0.0);
+    if (x < g.n[0] && y < g.n[1] && z < g.n[2]) {
+        const int wx = g.w[0], wy = g.w[1], wz = g.w[2];
+        const int zlo = max(z - (wz - 1), 0), zhi = min(z, g.nc[2] - 1);
+        for (int ia = 0; ia < wx; ++ia) {
+            const int sx = x - ia;
+            if (sx < 0 || sx >= g.nc[0]) continue;
+            for (int ib = 0; ib < wy; ++ib) {
+                const int sy = y - ib;
+                if (sy < 0 || sy >= g.nc[1] || zlo > zhi) continue;
+                const int k0 = (sx * g.nc[1] + sy) * g.nc[2];
+                const int p0 = a.cell_start[k0 + zlo], p1 = a.cell_start[k0 + zhi + 1];
+                for (int p = p0; p < p1; ++p) {
+                    const double* w = a.src_w + (int64_t)p * 3 * W;
+                    const int ic = z - a.src_start[3 * (int64_t)p + 2];
+                    const double wgt = (w[ia] * w[W + ib]) * w[2 * W + ic];
+                    const cplx qv = a.q_sorted[p];
+                    acc.re += wgt * qv.re;
+                    acc.im += wgt * qv.im;
+                }
+            }
+        }
+    }
+    a.work[t] = acc;
+}
+
+void launch_near_project(const EvalArgs& a, cudaStream_t s) {
+    const int W = a.g.order + 1;
+    const int b = nblk(a.n_fft, 256);
+    switch (W) {
+        case 2: k_near_project<2><<<b, 256, 0, s>>>(a); break;
+        case 3: k_near_project<3><<<b, 256, 0, s>>>(a); break;
+        case 4: k_near_project<4><<<b, 256, 0, s>>>(a); break;
+        case 5: k_near_project<5><<<b, 256, 0, s>>>(a); break;
+        case 6: k_near_project<6><<<b, 256, 0, s>>>(a); break;
+        default: k_near_project<7><<<b, 256, 0, s>>>(a); break;
+    }
+    fftpim_count_launch();
+}
+
+// ---------------------------------------------------------------- K2
+__global__ void k_spectrum_mul(cplx* __restrict__ work, const cplx* __restrict__ khat, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) work[i] = work[i] * khat[i];
+}
+void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s) {
+    k_spectrum_mul<<<nblk(a.n_fft, 256), 256, 0, s>>>(a.work, a.khat, a.n_fft);
+    fftpim_count_launch();
+}
+
+// ---------------------------------------------------------------- K5a
+// Each warp scatters its contiguous chunk of points into a private copy of the
+// far source grid in shared memory (lanes own distinct taps of one point, so
+// no collisions); warps are summed in order, blocks in order by k_far_reduce.
+__global__ void k_far_project(EvalArgs a) {
+    extern __shared__ cplx sgrid[];
+    const int nfx = a.fs.n[0], nfy = a.fs.n[1], nfz = a.fs.n[2];
+    const int nf = nfx * nfy * nfz;
+    const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = threadIdx.x; t < nf * warps; t += blockDim.x) sgrid[t] = mk(0.0);
+    __syncthreads();
+    cplx* mine = sgrid + warp * nf;
+    const int Wf = a.fs.order + 1;
+    const int wx = a.fs.w[0], wy = a.fs.w[1], wz = a.fs.w[2];
+    const int taps = wx * wy * wz;
+    const int64_t gw = (int64_t)blockIdx.x * warps + warp, nw = (int64_t)gridDim.x * warps;
+    const int64_t chunk = (a.N + nw - 1) / nw;
+    const int64_t p0 = gw * chunk, p1 = min(a.N, p0 + chunk);
+    for (int64_t p = p0; p < p1; ++p) {
+        const double* w = a.src_fw + p * 3 * Wf;
+        const int* st = a.src_fstart + 3 * p;
+        const cplx qv = a.q_sorted[p];
+        for (int tp = lane; tp < taps; tp += 32) {
+            const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+            const double wgt = (w[ia] * w[Wf + ib]) * w[2 * Wf + ic];
+            const int node = ((st[0] + ia) * nfy + (st[1] + ib)) * nfz + (st[2] + ic);
+            mine[node].re += wgt * qv.re;
+            mine[node].im += wgt * qv.im;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nf; t += blockDim.x) {
+        cplx s = mk(0.0);
+        for (int k = 0; k < warps; ++k) s = s + sgrid[k * nf + t];
+        a.far_partial[(int64_t)blockIdx.x * nf + t] = s;
+    }
+}
+
+__global__ void k_far_reduce(const cplx* __restrict__ partial, int blocks, int nf, cplx* __restrict__ qg) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nf) return;
+    cplx s = mk(0.0);
+    for (int b = 0; b < blocks; ++b) s = s + partial[(int64_t)b * nf + t];
+    qg[t] = s;
+}
+
+void launch_far_project(const EvalArgs& a, cudaStream_t s) {
+    const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
+    const size_t smem = (size_t)nf * a.far_warps * sizeof(cplx);
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_far_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    k_far_project<<<a.far_blocks, 32 * a.far_warps, smem, s>>>(a);
+    k_far_reduce<<<nblk(nf, 128), 128, 0, s>>>(a.far_partial, a.far_blocks, nf, a.far_qg);
+    fftpim_count_launch(2);
+}
+
+// ---------------------------------------------------------------- K5b
+// ug[o] = sum_s K[o - s + (n-1)] qg[s]; one warp per observer-grid node
+__global__ void k_far_sum(EvalArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nx = a.fs.n[0], ny = a.fs.n[1], nz = a.fs.n[2];
+    const int nf = nx * ny * nz;
+    if (o >= nf) return;
+    const int kx = 2 * nx - 1, ky = 2 * ny - 1, kz = 2 * nz - 1;
+    (void)kx;
+    const int oz = o % nz, oy = (o / nz) % ny, ox = o / (ny * nz);
+    cplx acc = mk(0.0);
+    for (int s = lane; s < nf; s += 32) {
+        const int sz = s % nz, sy = (s / nz) % ny, sx = s / (ny * nz);
+        const int idx = ((ox - sx + nx - 1) * ky + (oy - sy + ny - 1)) * kz + (oz - sz + nz - 1);
+        acc = acc + a.far_kernel[idx] * a.far_qg[s];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) a.far_ug[o] = acc;
+}
+
+void launch_far_sum(const EvalArgs& a, cudaStream_t s) {
+    const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
+    k_far_sum<<<nblk((int64_t)nf * 32, 256), 256, 0, s>>>(a);
+    fftpim_count_launch();
+}
+
+// ---------------------------------------------------------------- K3 + K4 + K5c
+template <int W, int WF, bool REAL>
+__global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (i >= a.M) return;
+    cplx acc = mk(0.0);
+    if (a.parts & FFTPIM_NEAR) {
+        // near interpolation from the inverse-FFT buffer (top corner of the padded grid)
+        const double* w = a.obs_w + i * 3 * W;
+        const int* st = a.obs_start + 3 * i;
+        const int wx = a.g.w[0], wy = a.g.w[1], wz = a.g.w[2];
+        const int taps = wx * wy * wz;
+        const int c1 = a.cdims[1], c2 = a.cdims[2];
+        for (int tp = lane; tp < taps; tp += 32) {
+            const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+            const double wgt = (w[ia] * w[W + ib]) * w[2 * W + ic];
+            const int64_t g = ((int64_t)(st[0] + ia) * c1 + (st[1] + ib)) * c2 + (st[2] + ic);
+            const cplx v = a.work[g];
+            acc.re += wgt * v.re;
+            acc.im += wgt * v.im;
+        }
+        // precorrection: u += sum coef * q[src]
+        const int64_t p0 = a.pair_ptr[i], p1 = a.pair_ptr[i + 1];
+        for (int64_t p = p0 + lane; p < p1; p += 32) {
+            const cplx qv = a.q_sorted[a.pair_src[p]];
+            if (REAL) {
+                const double c = a.coef_r[p];
+                acc.re += c * qv.re;
+                acc.im += c * qv.im;
+            } else {
+                acc = acc + a.coef[p] * qv;
+            }
+        }
+    }
+    if (a.parts & FFTPIM_FAR) {
+        const double* w = a.obs_fw + i * 3 * WF;
+        const int* st = a.obs_fstart + 3 * i;
+        const int wx = a.fo.w[0], wy = a.fo.w[1], wz = a.fo.w[2];
+        const int taps = wx * wy * wz;
+        const int ny = a.fo.n[1], nz = a.fo.n[2];
+        for (int tp = lane; tp < taps; tp += 32) {
+            const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+            const double wgt = (w[ia] * w[WF + ib]) * w[2 * WF + ic];
+            const cplx v = a.far_ug[((st[0] + ia) * ny + (st[1] + ib)) * nz + (st[2] + ic)];
+            acc.re += wgt * v.re;
+            acc.im += wgt * v.im;
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) a.u[a.obs_perm[i]] = acc;
+}
+
+template <int W, int WF>
+static void obs_dispatch_real(const EvalArgs& a, int blocks, cudaStream_t s) {
+    if (a.coef_r)
+        k_observers<W, WF, true><<<blocks, 256, 0, s>>>(a);
+    else
+        k_observers<W, WF, false><<<blocks, 256, 0, s>>>(a);
+}
+
+template <int W>
+static void obs_dispatch_far(const EvalArgs& a, int blocks, cudaStream_t s) {
+    switch (a.fo.order + 1) {
+        case 2: obs_dispatch_real<W, 2>(a, blocks, s); break;
+        case 3: obs_dispatch_real<W, 3>(a, blocks, s); break;
+        case 4: obs_dispatch_real<W, 4>(a, blocks, s); break;
+        case 5: obs_dispatch_real<W, 5>(a, blocks, s); break;
+        case 6: obs_dispatch_real<W, 6>(a, blocks, s); break;
+        default: obs_dispatch_real<W, 7>(a, blocks, s); break;
+    }
+}
+
+void launch_observers(const EvalArgs& a, cudaStream_t s) {
+    if (a.M == 0) return;
+    const int blocks = nblk(a.M * 32, 256);
+    switch (a.g.order + 1) {
+        case 2: obs_dispatch_far<2>(a, blocks, s); break;
+        case 3: obs_dispatch_far<3>(a, blocks, s); break;
+        case 4: obs_dispatch_far<4>(a, blocks, s); break;
+        case 5: obs_dispatch_far<5>(a, blocks, s); break;
+        case 6: obs_dispatch_far<6>(a, blocks, s); break;
+        default: obs_dispatch_far<7>(a, blocks, s); break;
+    }
+    fftpim_count_launch();
+}

@@ -1,0 +1,974 @@
+// fftpim.cu -- C ABI (include/fftpim.h): plan build orchestration on device,
+// evaluation, operand export.  The host code here only sets up scalars and
+// launches kernels; every O(N) or O(pairs) step runs on the GPU.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+#define CK(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess)                                                                     \
+            throw Fail{FFTPIM_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};              \
+    } while (0)
+#define CKFFT(x)                                                                                   \
+    do {                                                                                           \
+        cufftResult r_ = (x);                                                                      \
+        if (r_ != CUFFT_SUCCESS) throw Fail{FFTPIM_CUDA, std::string(#x) + ": cufft error " + std::to_string((int)r_)}; \
+    } while (0)
+
+template <typename T>
+T* dalloc(FftpimPlan* P, int64_t count) {
+    if (count <= 0) count = 1;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(T) * (size_t)count));
+    P->allocations.push_back(p);
+    P->device_bytes += (int64_t)(sizeof(T) * (size_t)count);
+    return (T*)p;
+}
+
+void dfree(FftpimPlan* P, void* p) {
+    if (!p) return;
+    auto it = std::find(P->allocations.begin(), P->allocations.end(), p);
+    if (it != P->allocations.end()) P->allocations.erase(it);
+    cudaFree(p);
+}
+
+// Golub-Welsch for the generalized Gauss-Laguerre rule with weight v^-1/2 e^-v
+// (special.py:53-63): eigen-decomposition of the symmetric tridiagonal Jacobi
+// matrix by implicit QL, tracking only the first eigenvector components.
+GLTable gauss_laguerre_half() {
+    const int n = FFTPIM_GL_N;
+    std::vector<double> d(n), e(n, 0.0), z(n, 0.0);
+    for (int k = 0; k < n; ++k) d[k] = 2.0 * k + 0.5;
+    for (int k = 1; k < n; ++k) e[k - 1] = std::sqrt(k * (k - 0.5));
+    z[0] = 1.0;   // first row of the eigenvector matrix, rotated along
+    for (int l = 0; l < n; ++l) {
+        int iter = 0;
+        while (true) {
+            int m = l;
+            for (; m < n - 1; ++m) {
+                double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+                if (std::fabs(e[m]) <= 1e-17 * dd) break;
+            }
+            if (m == l) break;
+            if (++iter > 200) break;
+            double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+            double r = std::hypot(g, 1.0);
+            g = d[m] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(r) : -std::fabs(r)));
+            double s = 1.0, c = 1.0, p = 0.0;
+            int i = m - 1;
+            for (; i >= l; --i) {
+                double f = s * e[i], b = c * e[i];
+                r = std::hypot(f, g);
+                e[i + 1] = r;
+                if (r == 0.0) {
+                    d[i + 1] -= p;
+                    e[m] = 0.0;
+                    break;
+                }
+                s = f / r;
+                c = g / r;
+                g = d[i + 1] - p;
+                r = (d[i] - g) * s + 2.0 * c * b;
+                p = s * r;
+                d[i + 1] = g + p;
+                g = c * r - b;
+                double fz = z[i + 1];
+                z[i + 1] = s * z[i] + c * fz;
+                z[i] = c * z[i] - s * fz;
+            }
+            if (r == 0.0 && i >= l) continue;
+            d[l] -= p;
+            e[l] = g;
+            e[m] = 0.0;
+        }
+    }
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
+    GLTable t;
+    for (int i = 0; i < n; ++i) {
+        t.node[i] = d[idx[i]];
+        t.weight[i] = std::sqrt(M_PI) * z[idx[i]] * z[idx[i]];
+    }
+    return t;
+}
+
+void set_geom(StencilGeom& g, const int n[3], const double origin[3], const double h[3], int order,
+              const double margin[3]) {
+    g.order = order;
+    for (int a = 0; a < 3; ++a) {
+        g.n[a] = n[a];
+        g.origin[a] = origin[a];
+        g.h[a] = h[a];
+        g.w[a] = n[a] > 1 ? order + 1 : 1;
+        g.nc[a] = n[a] - g.w[a] + 1;
+        g.margin[a] = margin[a];
+    }
+}
+
+void check_status(FftpimPlan* P, const char* phase) {
+    CK(cudaStreamSynchronize(P->build_stream));
+    DevStatus st;
+    CK(cudaMemcpy(&st, P->status, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st.code) {
+        char buf[256];
+        const char* what = "error";
+        switch (st.code) {
+            case FFTPIM_DOMAIN: what = "DomainError"; break;
+            case FFTPIM_WOOD_ANOMALY: what = "WoodAnomalyError"; break;
+            case FFTPIM_NOT_CONVERGED: what = "NotConvergedError"; break;
+            case FFTPIM_SEPARATION: what = "SeparationError"; break;
+        }
+        std::string detail;
+        switch (st.where) {
+            case 10: case 11: case 12: case 20: case 21: case 22: case 23:
+                detail = "point outside grid hull (beyond allowed margin)"; break;
+            case 30: detail = "observer " + std::to_string(st.a) + " coincides with a distinct source " +
+                              std::to_string(st.b) + " inside the error-correction region: true singularity"; break;
+            case 31: detail = "image point coincides with evaluation point (correction pair of observer " +
+                              std::to_string(st.a) + ")"; break;
+            case 40: case 42: detail = "1D series requires transverse separation sqrt(y^2+z^2) > 0"; break;
+            case 41: detail = "lattice series argument vanished"; break;
+            case 43: detail = "|k_rho(m=" + std::to_string(st.a) + ")| below threshold"; break;
+            case 44: detail = "|k_z(m=" + std::to_string(st.a) + ", n=" + std::to_string(st.b) + ")| below threshold"; break;
+            case 45: detail = "z image stack diverges: |exp(-j(k_z -+ k_z0) L_z)| > 1"; break;
+            case 46: detail = "resonant z stack at (m=" + std::to_string(st.a) + ", n=" + std::to_string(st.b) + ")"; break;
+            case 47: detail = "far kernel series did not converge at difference point " + std::to_string(st.a) +
+                              " (terms used: " + std::to_string(st.b) + ")"; break;
+            case 48: detail = "far kernel: image point coincides with evaluation point"; break;
+            default: detail = "code " + std::to_string(st.where);
+        }
+        snprintf(buf, sizeof(buf), "%s during %s: ", what, phase);
+        throw Fail{st.code, std::string(buf) + detail};
+    }
+}
+
+int64_t prod3(const int d[3]) { return (int64_t)d[0] * d[1] * d[2]; }
+
+template <typename K, typename V>
+void radix_sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int64_t n, int end_bit, cudaStream_t s) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, s);
+    void* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, bytes + 16, s));
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, s);
+    CK(cudaFreeAsync(tmp, s));
+    fftpim_count_launch(4);
+}
+
+int bits_for(int64_t maxval) {
+    int b = 1;
+    while (b < 31 && ((int64_t)1 << b) <= maxval) ++b;
+    return b;
+}
+
+// Sort points by near stencil cell; returns perm (sorted -> original), and
+// fills stencil arrays in sorted order.
+void sort_points(FftpimPlan* P, const double* d_pos, int64_t n, int* perm, int* cell_start_or_null,
+                 cudaStream_t s) {
+    const StencilGeom& g = P->near_g;
+    int64_t ncells = prod3(g.nc);
+    int* keys = nullptr;
+    int* keys_sorted = nullptr;
+    int* iota = nullptr;
+    CK(cudaMallocAsync(&keys, sizeof(int) * std::max<int64_t>(n, 1), s));
+    CK(cudaMallocAsync(&keys_sorted, sizeof(int) * std::max<int64_t>(n, 1), s));
+    CK(cudaMallocAsync(&iota, sizeof(int) * std::max<int64_t>(n, 1), s));
+    launch_cell_keys(d_pos, n, g, keys, P->status, s);
+    launch_iota(iota, n, s);
+    radix_sort_pairs(keys, keys_sorted, iota, perm, n, bits_for(ncells), s);
+    if (cell_start_or_null) launch_csr_from_sorted(keys_sorted, n, ncells, cell_start_or_null, s);
+    CK(cudaFreeAsync(keys, s));
+    CK(cudaFreeAsync(keys_sorted, s));
+    CK(cudaFreeAsync(iota, s));
+}
+
+void build(FftpimPlan* P) {
+    const FftpimProblem& pr = P->prob;
+    cudaStream_t s = P->build_stream;
+    const int64_t N = pr.n_src, M = pr.n_obs;
+    P->N = N;
+    P->M = M;
+    P->npsp = pr.regime == FFTPIM_NPSP;
+    if (N <= 0 || M <= 0) throw Fail{FFTPIM_VALUE, "empty source or observer set"};
+    if (pr.i_d < 1) throw Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"};
+    if (pr.dim < 1 || pr.dim > 3) throw Fail{FFTPIM_VALUE, "dim must be 1, 2 or 3"};
+    if (pr.near_order < 1 || pr.near_order > FFTPIM_MAX_ORDER || pr.far_order < 1 ||
+        pr.far_order > FFTPIM_MAX_ORDER)
+        throw Fail{FFTPIM_VALUE, "interpolation order must be in [1, 6]"};
+    if (pr.i_d > 2) throw Fail{FFTPIM_VALUE, "i_d > 2 is not supported by this build"};
+
+    // ---- near grid (nearzone.py:198-211, grids.py:90-107)
+    int dims[3];
+    bool auto_grid = pr.near_grid[0] <= 0 && pr.near_grid[1] <= 0 && pr.near_grid[2] <= 0;
+    if (auto_grid) {   // model.py:146-162
+        int act = 0;
+        for (int a = 0; a < 3; ++a) act += pr.D[a] > 0.0;
+        double target = 1.15 * (double)std::max<int64_t>(std::max(N, M), 1);
+        int side = std::max(2, (int)std::ceil(std::pow(target, 1.0 / act)));
+        if (side % 2 == 0) ++side;
+        for (int a = 0; a < 3; ++a) dims[a] = pr.D[a] > 0.0 ? side : 1;
+    } else {
+        for (int a = 0; a < 3; ++a) dims[a] = pr.D[a] > 0.0 ? pr.near_grid[a] : 1;
+    }
+    double h[3], zero3[3] = {0, 0, 0};
+    for (int a = 0; a < 3; ++a) {
+        if (pr.D[a] > 0.0 && dims[a] < 2)
+            throw Fail{FFTPIM_VALUE, "near grid needs >= 2 points on active axis " + std::to_string(a)};
+        h[a] = pr.D[a] > 0.0 ? pr.D[a] / (dims[a] - 1) : 0.0;
+        if (dims[a] > 1 && pr.near_order + 1 > dims[a])
+            throw Fail{FFTPIM_VALUE, "near order needs more planes than the grid has"};
+    }
+    int nb[3];
+    for (int a = 0; a < 3; ++a) nb[a] = std::max(dims[a] - 1, 1);
+    for (int a = 0; a < pr.dim; ++a)
+        if (dims[a] > 1 && 2.0 * pr.er_range_boxes * h[a] >= pr.L[a])
+            throw Fail{FFTPIM_VALUE, "error-correction range on axis " + std::to_string(a) +
+                                         " must satisfy 2*D_ER < L"};
+    double margin[3];
+    for (int a = 0; a < 3; ++a) margin[a] = 1e-9 * std::max(h[a], 1.0);   // nearzone.py:237
+    set_geom(P->near_g, dims, zero3, h, pr.near_order, margin);
+    P->n_grid = prod3(dims);
+    for (int a = 0; a < 3; ++a) P->cdims[a] = dims[a] > 1 ? 2 * dims[a] : 1;
+    P->n_fft = prod3(P->cdims);
+
+    // ---- far grids (grids.py:58-87, farzone.py:84-98, 125-127)
+    int fdims[3];
+    double fs_org[3], fo_org[3], fh[3], fmarg[3];
+    for (int a = 0; a < 3; ++a) {
+        if (pr.D[a] <= 0.0) {
+            fdims[a] = 1;
+            fs_org[a] = fo_org[a] = fh[a] = 0.0;
+            continue;
+        }
+        fdims[a] = pr.far_grid[a];
+        if (fdims[a] < 2) throw Fail{FFTPIM_VALUE, "far grid needs >= 2 points on active axis"};
+        if (pr.far_order + 1 > fdims[a]) throw Fail{FFTPIM_VALUE, "far order needs more planes than the grid has"};
+        fh[a] = pr.D[a] / fdims[a];
+        fs_org[a] = 0.0;
+        fo_org[a] = fh[a] / 2.0;
+    }
+    P->info.on_axis_offset = 0;
+    if (pr.dim == 1 && pr.D[1] == 0.0 && pr.D[2] == 0.0) {
+        fs_org[1] = fh[0] / 2.0;
+        P->info.on_axis_offset = 1;
+    }
+    for (int a = 0; a < 3; ++a) fmarg[a] = fdims[a] > 1 ? fh[a] : 0.0;
+    set_geom(P->far_sg, fdims, fs_org, fh, pr.far_order, fmarg);
+    set_geom(P->far_og, fdims, fo_org, fh, pr.far_order, fmarg);
+    P->n_far = prod3(fdims);
+    for (int a = 0; a < 3; ++a) P->far_kdims[a] = fdims[a] > 1 ? 2 * fdims[a] - 1 : 1;
+
+    // ---- images of G_near (pgf.py:114-123)
+    ImageSet& im = P->images;
+    im.k0_re = pr.k0[0];
+    im.k0_im = pr.k0[1];
+    double maxL = std::max(pr.L[0], std::max(pr.L[1], pr.L[2]));
+    double maxD = std::max(pr.D[0], std::max(pr.D[1], pr.D[2]));
+    double maxLp = 0.0;
+    for (int a = 0; a < pr.dim; ++a) maxLp = std::max(maxLp, pr.L[a]);
+    im.sing_tol = 1e-12 * std::max(std::max(maxL, maxD), 1.0);   // nearzone.py:213
+    im.sep_tol = 1e-13 * std::max(maxLp, 1.0);                     // pgf.py:93-94
+    {
+        int hw[3];
+        for (int a = 0; a < 3; ++a) hw[a] = a < pr.dim ? pr.i_d : 0;
+        int c = 0;
+        std::complex<double> kl[3];
+        for (int a = 0; a < 3; ++a) kl[a] = std::complex<double>(pr.kshift[a][0], pr.kshift[a][1]) * pr.L[a];
+        for (int i = -hw[0]; i <= hw[0]; ++i)
+            for (int j = -hw[1]; j <= hw[1]; ++j)
+                for (int k = -hw[2]; k <= hw[2]; ++k) {
+                    double idx[3] = {(double)i, (double)j, (double)k};
+                    std::complex<double> dotp = idx[0] * kl[0] + idx[1] * kl[1] + idx[2] * kl[2];
+                    std::complex<double> ph = std::exp(std::complex<double>(0.0, -1.0) * dotp);
+                    for (int a = 0; a < 3; ++a) im.off[c][a] = idx[a] * pr.L[a];
+                    im.ph_re[c] = ph.real();
+                    im.ph_im[c] = ph.imag();
+                    ++c;
+                }
+        im.count = c;
+    }
+
+    // ---- points
+    double* d_src = dalloc<double>(P, 3 * N);
+    CK(cudaMemcpyAsync(d_src, pr.src_pos, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, s));
+    double* d_obs = d_src;
+    const bool same = pr.same_points != 0;
+    if (!same) {
+        d_obs = dalloc<double>(P, 3 * M);
+        CK(cudaMemcpyAsync(d_obs, pr.obs_pos, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
+    }
+    const int W = pr.near_order + 1, WF = pr.far_order + 1;
+    P->src_perm = dalloc<int>(P, N);
+    P->src_rank = dalloc<int>(P, N);
+    P->cell_start = dalloc<int>(P, prod3(P->near_g.nc) + 1);
+    sort_points(P, d_src, N, P->src_perm, P->cell_start, s);
+    launch_rank(P->src_perm, N, P->src_rank, s);
+    P->src_w = dalloc<double>(P, N * 3 * W);
+    P->src_start = dalloc<int>(P, N * 3);
+    launch_stencils(d_src, P->src_perm, N, P->near_g, P->src_w, P->src_start, P->status, 20, s);
+    P->src_fw = dalloc<double>(P, N * 3 * WF);
+    P->src_fstart = dalloc<int>(P, N * 3);
+    launch_stencils(d_src, P->src_perm, N, P->far_sg, P->src_fw, P->src_fstart, P->status, 21, s);
+    if (same) {
+        P->obs_perm = P->src_perm;
+        P->obs_w = P->src_w;
+        P->obs_start = P->src_start;
+    } else {
+        P->obs_perm = dalloc<int>(P, M);
+        sort_points(P, d_obs, M, P->obs_perm, nullptr, s);
+        P->obs_w = dalloc<double>(P, M * 3 * W);
+        P->obs_start = dalloc<int>(P, M * 3);
+        launch_stencils(d_obs, P->obs_perm, M, P->near_g, P->obs_w, P->obs_start, P->status, 22, s);
+    }
+    P->obs_fw = dalloc<double>(P, M * 3 * WF);
+    P->obs_fstart = dalloc<int>(P, M * 3);
+    launch_stencils(d_obs, P->obs_perm, M, P->far_og, P->obs_fw, P->obs_fstart, P->status, 23, s);
+    check_status(P, "stencil construction");
+
+    // ---- near kernel table -> kernel_hat (nearzone.py:215-235)
+    P->khat = dalloc<cplx>(P, P->n_fft);
+    launch_embed_table(P->khat, P->cdims, dims, h, im, s);
+    unsigned long long* d_cnt = dalloc<unsigned long long>(P, 4);
+    CK(cudaMemsetAsync(d_cnt, 0, 4 * sizeof(unsigned long long), s));
+    launch_count_coincident(dims, h, im, d_cnt, s);
+    {
+        int rank = 0, n[3];
+        for (int a = 0; a < 3; ++a)
+            if (P->cdims[a] > 1) n[rank++] = P->cdims[a];
+        if (rank == 0) throw Fail{FFTPIM_VALUE, "near grid has no active axis"};
+        CKFFT(cufftPlanMany(&P->fft_plan, rank, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 1));
+        CKFFT(cufftSetStream(P->fft_plan, s));
+        CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->khat, (cufftDoubleComplex*)P->khat, CUFFT_FORWARD));
+        fftpim_count_launch(1);
+        launch_scale(P->khat, P->n_fft, 1.0 / (double)P->n_fft, s);   // numpy ifftn's 1/M
+    }
+    P->work = dalloc<cplx>(P, P->n_fft);
+    P->q_sorted = dalloc<cplx>(P, N);
+
+    // ---- correction pairs (nearzone.py:245-256, 303-487)
+    PairGeom& pg = P->pg;
+    const int jr_full = pr.er_range_boxes + pr.near_order + 2;
+    int jr[3], pad[3];
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] == 1) {
+            jr[a] = 0;
+        } else {
+            int r = jr_full;
+            if (a < pr.dim) {
+                int per = (int)std::floor(pr.L[a] / h[a] + 1e-9);
+                int half = (per - 1 >= 0) ? (per - 1) / 2 : -((2 - per) / 2);   // Python floor division
+                r = std::min(r, std::max(half, 1));
+            }
+            jr[a] = std::min(r, nb[a]);
+        }
+        pad[a] = jr[a] + 1;
+    }
+    int max_pad = std::max(pad[0], std::max(pad[1], pad[2]));
+    for (int a = 0; a < 3; ++a) {
+        pg.dims[a] = dims[a];
+        pg.h[a] = h[a];
+        pg.inv_h[a] = dims[a] > 1 ? 1.0 / h[a] : 0.0;
+        pg.nb[a] = nb[a];
+        pg.jr[a] = jr[a];
+        pg.ext[a] = dims[a] > 1 ? nb[a] + 2 * max_pad : 1;
+        P->info.join_radius[a] = jr[a];
+    }
+    P->info.jr_full = jr_full;
+    pg.max_pad = max_pad;
+    pg.r2_keep = (double)jr_full * (double)jr_full + 1e-9;
+    pg.sing_tol = im.sing_tol;
+    pg.same_points = same;
+    // code list: (0,0,0) first, then itertools.product order (nearzone.py:315-319)
+    {
+        int c = 0;
+        auto set_code = [&](int cx, int cy, int cz) {
+            pg.code[c][0] = cx;
+            pg.code[c][1] = cy;
+            pg.code[c][2] = cz;
+            std::complex<double> dotp(0.0, 0.0);
+            for (int a = 0; a < 3; ++a) {
+                double cv = (double)pg.code[c][a];
+                pg.shift[c][a] = cv * pr.L[a];
+                dotp += cv * (std::complex<double>(pr.kshift[a][0], pr.kshift[a][1]) * pr.L[a]);
+            }
+            std::complex<double> ph = std::exp(std::complex<double>(0.0, -1.0) * dotp);
+            pg.phase_re[c] = ph.real();
+            pg.phase_im[c] = ph.imag();
+            ++c;
+        };
+        set_code(0, 0, 0);
+        int rng[3][2];
+        for (int a = 0; a < 3; ++a) {
+            bool wrap = a < pr.dim && dims[a] > 1;
+            rng[a][0] = wrap ? -1 : 0;
+            rng[a][1] = wrap ? 1 : 0;
+        }
+        for (int cx = rng[0][0]; cx <= rng[0][1]; ++cx)
+            for (int cy = rng[1][0]; cy <= rng[1][1]; ++cy)
+                for (int cz = rng[2][0]; cz <= rng[2][1]; ++cz)
+                    if (cx || cy || cz) set_code(cx, cy, cz);
+        pg.ncodes = c;
+    }
+    // augmented source list: originals, then wrapped copies code by code
+    std::vector<int64_t> code_off(pg.ncodes + 1, 0);
+    int* aug_orig = nullptr;
+    unsigned char* aug_code = nullptr;
+    int64_t A = N;
+    {
+        std::vector<int*> parts;
+        std::vector<int64_t> counts;
+        unsigned char* flags = nullptr;
+        int* d_nsel = nullptr;
+        CK(cudaMallocAsync(&flags, N, s));
+        CK(cudaMallocAsync(&d_nsel, sizeof(int), s));
+        code_off[0] = 0;
+        code_off[1] = N;
+        for (int c = 1; c < pg.ncodes; ++c) {
+            int cv[3];
+            double lo[3], hi[3];
+            for (int a = 0; a < 3; ++a) {
+                cv[a] = pg.code[c][a];
+                double pd = pad[a] * h[a];
+                lo[a] = pr.L[a] - pd;
+                hi[a] = pr.D[a] - pr.L[a] + pd;
+            }
+            launch_wrap_flags(d_src, N, cv, lo, hi, flags, s);
+            int* sel = nullptr;
+            CK(cudaMallocAsync(&sel, sizeof(int) * N, s));
+            size_t bytes = 0;
+            cub::CountingInputIterator<int> it(0);
+            cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, sel, d_nsel, (int)N, s);
+            void* tmp = nullptr;
+            CK(cudaMallocAsync(&tmp, bytes + 16, s));
+            cub::DeviceSelect::Flagged(tmp, bytes, it, flags, sel, d_nsel, (int)N, s);
+            fftpim_count_launch(2);
+            CK(cudaFreeAsync(tmp, s));
+            int nsel = 0;
+            CK(cudaMemcpyAsync(&nsel, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            parts.push_back(sel);
+            counts.push_back(nsel);
+            code_off[c + 1] = code_off[c] + nsel;
+        }
+        A = code_off[pg.ncodes];
+        aug_orig = dalloc<int>(P, A);
+        aug_code = dalloc<unsigned char>(P, A);
+        launch_iota(aug_orig, N, s);
+        launch_fill_u8(aug_code, N, 0, s);
+        for (int c = 1; c < pg.ncodes; ++c) {
+            int64_t n = counts[c - 1];
+            if (n)
+                CK(cudaMemcpyAsync(aug_orig + code_off[c], parts[c - 1], sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+            launch_fill_u8(aug_code + code_off[c], n, (unsigned char)c, s);
+            CK(cudaFreeAsync(parts[c - 1], s));
+        }
+        CK(cudaFreeAsync(flags, s));
+        CK(cudaFreeAsync(d_nsel, s));
+    }
+    // bucket augmented sources by padded box (stable: reference aug order inside a box)
+    int64_t total_boxes = (int64_t)pg.ext[0] * pg.ext[1] * pg.ext[2];
+    if (total_boxes >= INT_MAX) throw Fail{FFTPIM_VALUE, "too many correction boxes"};
+    int* box_start = dalloc<int>(P, total_boxes + 1);
+    int* box_order = dalloc<int>(P, A);
+    {
+        int *keys = nullptr, *keys_sorted = nullptr, *iota = nullptr;
+        CK(cudaMallocAsync(&keys, sizeof(int) * A, s));
+        CK(cudaMallocAsync(&keys_sorted, sizeof(int) * A, s));
+        CK(cudaMallocAsync(&iota, sizeof(int) * A, s));
+        launch_aug_keys(d_src, aug_orig, aug_code, A, pg, keys, s);
+        launch_iota(iota, A, s);
+        radix_sort_pairs(keys, keys_sorted, iota, box_order, A, bits_for(total_boxes), s);
+        launch_csr_from_sorted(keys_sorted, A, total_boxes, box_start, s);
+        CK(cudaFreeAsync(keys, s));
+        CK(cudaFreeAsync(keys_sorted, s));
+        CK(cudaFreeAsync(iota, s));
+    }
+    // count pass
+    PairArgs pa{};
+    pa.src_pos = d_src;
+    pa.obs_pos = d_obs;
+    pa.obs_perm = P->obs_perm;
+    pa.M = M;
+    pa.box_start = box_start;
+    pa.box_order = box_order;
+    pa.aug_orig = aug_orig;
+    pa.aug_code = aug_code;
+    pa.obs_start = P->obs_start;
+    pa.obs_w = P->obs_w;
+    pa.src_start = P->src_start;
+    pa.src_w = P->src_w;
+    pa.src_rank = P->src_rank;
+    pa.W = W;
+    for (int a = 0; a < 3; ++a) pa.wdt[a] = P->near_g.w[a];
+    pa.st = P->status;
+    int64_t* counts = dalloc<int64_t>(P, M + 1);
+    int* d0mm = dalloc<int>(P, 2 * 81);
+    {
+        std::vector<int> init(162);
+        for (int i = 0; i < 81; ++i) {
+            init[i] = INT_MAX;
+            init[81 + i] = INT_MIN;
+        }
+        CK(cudaMemcpyAsync(d0mm, init.data(), sizeof(int) * 162, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    pa.counts = counts;
+    pa.d0min = d0mm;
+    pa.d0max = d0mm + 81;
+    pa.tallies = d_cnt + 1;
+    launch_pairs_count(pg, pa, s);
+    check_status(P, "correction pair discovery");
+    P->pair_ptr = dalloc<int64_t>(P, M + 1);
+    {
+        size_t bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, P->pair_ptr, (int)(M + 1), s);
+        void* tmp = nullptr;
+        CK(cudaMallocAsync(&tmp, bytes + 16, s));
+        CK(cudaMemsetAsync(counts + M, 0, sizeof(int64_t), s));
+        cub::DeviceScan::ExclusiveSum(tmp, bytes, counts, P->pair_ptr, (int)(M + 1), s);
+        fftpim_count_launch(2);
+        CK(cudaFreeAsync(tmp, s));
+    }
+    int64_t npairs = 0;
+    unsigned long long tallies[3];
+    std::vector<int> mm(162);
+    CK(cudaMemcpyAsync(&npairs, P->pair_ptr + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(tallies, d_cnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(mm.data(), d0mm, sizeof(int) * 162, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    P->info.coincident_kernel_terms = (int64_t)tallies[0];
+    P->info.n_self_pairs = (int64_t)tallies[1];
+    P->info.n_wrapped_pairs = (int64_t)tallies[2];
+    P->info.n_pairs = npairs;
+    // window tables per code (values independent of the window, nearzone.py:439-451)
+    CodeTables& tb = P->tabs;
+    int64_t tab_total = 0;
+    for (int c = 0; c < 27; ++c) {
+        tb.offset[c] = tab_total;
+        for (int a = 0; a < 3; ++a) {
+            tb.lo[c][a] = 0;
+            tb.len[c][a] = 0;
+        }
+        if (c >= pg.ncodes || mm[c * 3] == INT_MAX) continue;
+        int64_t sz = 1;
+        for (int a = 0; a < 3; ++a) {
+            tb.lo[c][a] = mm[c * 3 + a];
+            tb.len[c][a] = mm[81 + c * 3 + a] + 2 * (P->near_g.w[a] - 1) - mm[c * 3 + a] + 1;
+            sz *= tb.len[c][a];
+        }
+        tab_total += sz;
+    }
+    cplx* tables = dalloc<cplx>(P, tab_total);
+    launch_code_tables(tb, pg.ncodes, pg, im, tables, tab_total, s);
+    // fill pass
+    P->pair_src = dalloc<int>(P, npairs);
+    P->pair_codeid = dalloc<unsigned char>(P, npairs);
+    if (P->npsp)
+        P->pair_coef_r = dalloc<double>(P, npairs);
+    else
+        P->pair_coef = dalloc<cplx>(P, npairs);
+    P->info.real_coefficients = P->npsp ? 1 : 0;
+    pa.pair_ptr = P->pair_ptr;
+    pa.tables = tables;
+    pa.pair_src = P->pair_src;
+    pa.pair_codeid = P->pair_codeid;
+    pa.coef = P->pair_coef;
+    pa.coef_r = P->pair_coef_r;
+    launch_pairs_fill(pg, im, tb, pa, s);
+    check_status(P, "correction coefficients");
+    CK(cudaStreamSynchronize(s));
+    dfree(P, tables);
+    dfree(P, counts);
+    dfree(P, d0mm);
+    dfree(P, box_start);
+    dfree(P, box_order);
+    dfree(P, aug_orig);
+    dfree(P, aug_code);
+
+    // ---- far kernel (farzone.py:100-121, pgf.py:450-462)
+    {
+        std::vector<double> axes;
+        double zmin = 1e300, zmax = -1e300;
+        for (int a = 0; a < 3; ++a) {
+            int n = fdims[a];
+            double shift = P->far_og.origin[a] - P->far_sg.origin[a];
+            if (n == 1) {
+                axes.push_back(shift);
+                if (a == 2) zmin = zmax = shift;
+            } else {
+                for (int l = -(n - 1); l < n; ++l) {
+                    double v = (double)l * fh[a] + shift;
+                    axes.push_back(v);
+                    if (a == 2) {
+                        zmin = std::min(zmin, v);
+                        zmax = std::max(zmax, v);
+                    }
+                }
+            }
+        }
+        double* d_axes = dalloc<double>(P, (int64_t)axes.size());
+        CK(cudaMemcpyAsync(d_axes, axes.data(), sizeof(double) * axes.size(), cudaMemcpyHostToDevice, s));
+        FarSeriesParams fp{};
+        fp.dim = pr.dim;
+        fp.npsp = P->npsp;
+        for (int a = 0; a < 3; ++a) {
+            fp.L[a] = pr.L[a];
+            fp.ks_re[a] = pr.kshift[a][0];
+            fp.ks_im[a] = pr.kshift[a][1];
+        }
+        fp.k0_re = pr.k0[0];
+        fp.k0_im = pr.k0[1];
+        fp.tol = pr.series_tol;
+        fp.cutoff = std::log(1.0 / pr.series_tol) + 8.0;
+        fp.sep = im.sep_tol;
+        fp.wood = 1e-8 * 2.0 * M_PI / maxLp;
+        fp.zmin = zmin;
+        fp.zmax = zmax;
+        fp.max_terms = 1000000;
+        fp.max_layers = 200000;
+        GLTable gl = gauss_laguerre_half();
+        P->far_kernel = dalloc<cplx>(P, prod3(P->far_kdims));
+        launch_far_series(d_axes, P->far_kdims, fp, im, gl, P->far_kernel, P->status, s);
+        check_status(P, "far kernel tabulation");
+        DevStatus st;
+        CK(cudaMemcpy(&st, P->status, sizeof(st), cudaMemcpyDeviceToHost));
+        P->info.kernel_terms = st.kernel_terms;
+        dfree(P, d_axes);
+    }
+    // far evaluation scratch
+    {
+        const int64_t nf = P->n_far;
+        int warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (160 * 1024) / (nf * (int64_t)sizeof(cplx))));
+        if (nf * (int64_t)sizeof(cplx) > 200 * 1024) throw Fail{FFTPIM_VALUE, "far grid too large (max 12800 nodes)"};
+        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, (N + 32 * warps * 8 - 1) / (32 * warps * 8)));
+        P->far_warps = warps;
+        P->far_blocks = blocks;
+        P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
+        P->far_qg = dalloc<cplx>(P, nf);
+        P->far_ug = dalloc<cplx>(P, nf);
+    }
+    CK(cudaStreamSynchronize(s));
+    dfree(P, d_cnt);
+    dfree(P, d_src);
+    if (!same) dfree(P, d_obs);
+    for (int a = 0; a < 3; ++a) {
+        P->info.near_dims[a] = dims[a];
+        P->info.fft_dims[a] = P->cdims[a];
+        P->info.far_dims[a] = fdims[a];
+    }
+    P->info.n_src = N;
+    P->info.n_obs = M;
+}
+
+EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
+    EvalArgs a{};
+    a.N = P->N;
+    a.M = P->M;
+    a.q = (const cplx*)q;
+    a.u = (cplx*)u;
+    a.src_perm = P->src_perm;
+    a.obs_perm = P->obs_perm;
+    a.q_sorted = P->q_sorted;
+    a.g = P->near_g;
+    for (int i = 0; i < 3; ++i) a.cdims[i] = P->cdims[i];
+    a.cell_start = P->cell_start;
+    a.src_w = P->src_w;
+    a.src_start = P->src_start;
+    a.obs_w = P->obs_w;
+    a.obs_start = P->obs_start;
+    a.work = P->work;
+    a.khat = P->khat;
+    a.n_fft = P->n_fft;
+    a.pair_ptr = P->pair_ptr;
+    a.pair_src = P->pair_src;
+    a.coef = P->pair_coef;
+    a.coef_r = P->pair_coef_r;
+    a.fs = P->far_sg;
+    a.fo = P->far_og;
+    a.src_fw = P->src_fw;
+    a.src_fstart = P->src_fstart;
+    a.obs_fw = P->obs_fw;
+    a.obs_fstart = P->obs_fstart;
+    a.far_kernel = P->far_kernel;
+    a.far_partial = P->far_partial;
+    a.far_qg = P->far_qg;
+    a.far_ug = P->far_ug;
+    a.far_blocks = P->far_blocks;
+    a.far_warps = P->far_warps;
+    a.parts = parts;
+    return a;
+}
+
+void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s,
+              cudaEvent_t* ev = nullptr) {
+    if (parts & ~FFTPIM_ALL || parts == 0) throw Fail{FFTPIM_VALUE, "parts must be a non-empty subset of NEAR|FAR"};
+    CK(cudaSetDevice(P->device));
+    if (parts & FFTPIM_NEAR) CKFFT(cufftSetStream(P->fft_plan, s));
+    auto mark = [&](int k) {
+        if (ev) CK(cudaEventRecord(ev[k], s));
+    };
+    for (int64_t b = 0; b < batch; ++b) {
+        EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
+        mark(0);
+        launch_permute_q(a, s);
+        mark(1);
+        if (parts & FFTPIM_FAR) launch_far_project(a, s);
+        mark(2);
+        if (parts & FFTPIM_FAR) launch_far_sum(a, s);
+        mark(3);
+        if (parts & FFTPIM_NEAR) launch_near_project(a, s);
+        mark(4);
+        if (parts & FFTPIM_NEAR) {
+            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+            fftpim_count_launch(1);
+        }
+        mark(5);
+        if (parts & FFTPIM_NEAR) launch_spectrum_mul(a, s);
+        mark(6);
+        if (parts & FFTPIM_NEAR) {
+            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+            fftpim_count_launch(1);
+        }
+        mark(7);
+        launch_observers(a, s);
+        mark(8);
+    }
+    CK(cudaGetLastError());
+}
+
+int fail(const Fail& f) {
+    g_last_error = f.msg;
+    return f.code;
+}
+
+}  // namespace
+
+void fftpim_count_launch(int n) { g_launches += n; }
+
+extern "C" {
+
+int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out) {
+    if (!p || !out) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    *out = nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    FftpimPlan* P = new FftpimPlan();
+    try {
+        P->prob = *p;
+        P->device = p->device;
+        memset(&P->info, 0, sizeof(P->info));
+        CK(cudaSetDevice(P->device));
+        CK(cudaStreamCreateWithFlags(&P->build_stream, cudaStreamNonBlocking));
+        P->status = dalloc<DevStatus>(P, 1);
+        CK(cudaMemsetAsync(P->status, 0, sizeof(DevStatus), P->build_stream));
+        build(P);
+        P->prob.src_pos = nullptr;
+        P->prob.obs_pos = nullptr;
+        P->info.device_bytes = P->device_bytes;
+        P->info.build_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = P;
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        cudaStreamSynchronize(P->build_stream);
+        fftpim_plan_destroy(P);
+        return fail(f);
+    }
+}
+
+int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts, void* stream) {
+    if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    try {
+        evaluate(plan, q, u, batch, parts, (cudaStream_t)stream);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts) {
+    if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    try {
+        CK(cudaSetDevice(plan->device));
+        cudaStream_t s = plan->build_stream;
+        double *dq = nullptr, *du = nullptr;
+        size_t qb = sizeof(double) * 2 * plan->N * batch, ub = sizeof(double) * 2 * plan->M * batch;
+        CK(cudaMallocAsync(&dq, qb, s));
+        CK(cudaMallocAsync(&du, ub, s));
+        CK(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, s));
+        evaluate(plan, dq, du, batch, parts, s);
+        CK(cudaMemcpyAsync(u, du, ub, cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(dq, s));
+        CK(cudaFreeAsync(du, s));
+        CK(cudaStreamSynchronize(s));
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t parts, void* stream,
+                        double* stage_ms) {
+    if (!plan || !q || !u || !stage_ms) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    cudaEvent_t ev[FFTPIM_N_STAGES + 1] = {};
+    try {
+        CK(cudaSetDevice(plan->device));
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        evaluate(plan, q, u, 1, parts, (cudaStream_t)stream, ev);
+        CK(cudaEventSynchronize(ev[FFTPIM_N_STAGES]));
+        for (int k = 0; k < FFTPIM_N_STAGES; ++k) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+            stage_ms[k] = ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        return fail(f);
+    }
+}
+
+int fftpim_plan_info(const FftpimPlan* plan, FftpimInfo* info) {
+    if (!plan || !info) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    *info = plan->info;
+    return FFTPIM_OK;
+}
+
+int fftpim_plan_export(const FftpimPlan* cplan, int32_t which, void* dst, int64_t bytes) {
+    FftpimPlan* P = const_cast<FftpimPlan*>(cplan);
+    if (!P || !dst) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    try {
+        CK(cudaSetDevice(P->device));
+        const int64_t M = P->M, N = P->N, npairs = P->info.n_pairs;
+        auto need = [&](int64_t b) {
+            if (bytes < b) throw Fail{FFTPIM_VALUE, "export buffer too small: need " + std::to_string(b) + " bytes"};
+        };
+        if (which == FFTPIM_FAR_KERNEL) {
+            int64_t n = prod3(P->far_kdims);
+            need(n * 16);
+            CK(cudaMemcpy(dst, P->far_kernel, n * 16, cudaMemcpyDeviceToHost));
+            return FFTPIM_OK;
+        }
+        if (which == FFTPIM_KERNEL_HAT) {
+            need(P->n_fft * 16);
+            CK(cudaMemcpy(dst, P->khat, P->n_fft * 16, cudaMemcpyDeviceToHost));
+            double* d = (double*)dst;
+            for (int64_t i = 0; i < 2 * P->n_fft; ++i) d[i] *= (double)P->n_fft;
+            return FFTPIM_OK;
+        }
+        if (which < FFTPIM_PAIR_OBS || which > FFTPIM_PAIR_COEF) throw Fail{FFTPIM_VALUE, "unknown operand"};
+        std::vector<int64_t> ptr(M + 1);
+        std::vector<int> operm(M), sperm(N), psrc(npairs);
+        CK(cudaMemcpy(ptr.data(), P->pair_ptr, sizeof(int64_t) * (M + 1), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(operm.data(), P->obs_perm, sizeof(int) * M, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> orank(M);
+        for (int64_t i = 0; i < M; ++i) orank[operm[i]] = i;
+        // reference order: by original observer index
+        std::vector<int64_t> order;
+        order.reserve(npairs);
+        for (int64_t m = 0; m < M; ++m) {
+            int64_t i = orank[m];
+            for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) order.push_back(p);
+        }
+        if (which == FFTPIM_PAIR_OBS) {
+            need(npairs * 4);
+            int* o = (int*)dst;
+            int64_t k = 0;
+            for (int64_t m = 0; m < M; ++m) {
+                int64_t i = orank[m];
+                for (int64_t p = ptr[i]; p < ptr[i + 1]; ++p) o[k++] = (int)m;
+            }
+        } else if (which == FFTPIM_PAIR_SRC) {
+            need(npairs * 4);
+            CK(cudaMemcpy(psrc.data(), P->pair_src, sizeof(int) * npairs, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(sperm.data(), P->src_perm, sizeof(int) * N, cudaMemcpyDeviceToHost));
+            int* o = (int*)dst;
+            for (int64_t k = 0; k < npairs; ++k) o[k] = sperm[psrc[order[k]]];
+        } else if (which == FFTPIM_PAIR_CODE) {
+            need(npairs * 3);
+            std::vector<unsigned char> cid(npairs);
+            CK(cudaMemcpy(cid.data(), P->pair_codeid, npairs, cudaMemcpyDeviceToHost));
+            signed char* o = (signed char*)dst;
+            for (int64_t k = 0; k < npairs; ++k)
+                for (int a = 0; a < 3; ++a) o[3 * k + a] = P->pg.code[cid[order[k]]][a];
+        } else {
+            need(npairs * 16);
+            double* o = (double*)dst;
+            if (P->pair_coef_r) {
+                std::vector<double> c(npairs);
+                CK(cudaMemcpy(c.data(), P->pair_coef_r, sizeof(double) * npairs, cudaMemcpyDeviceToHost));
+                for (int64_t k = 0; k < npairs; ++k) {
+                    o[2 * k] = c[order[k]];
+                    o[2 * k + 1] = 0.0;
+                }
+            } else {
+                std::vector<cplx> c(npairs);
+                CK(cudaMemcpy(c.data(), P->pair_coef, sizeof(cplx) * npairs, cudaMemcpyDeviceToHost));
+                for (int64_t k = 0; k < npairs; ++k) {
+                    o[2 * k] = c[order[k]].re;
+                    o[2 * k + 1] = c[order[k]].im;
+                }
+            }
+        }
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_plan_set_far_kernel(FftpimPlan* plan, const double* kernel, int64_t n_entries) {
+    if (!plan || !kernel) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    try {
+        if (n_entries != prod3(plan->far_kdims)) throw Fail{FFTPIM_KERNEL_CACHE, "far kernel table size mismatch"};
+        CK(cudaSetDevice(plan->device));
+        CK(cudaMemcpy(plan->far_kernel, kernel, n_entries * 16, cudaMemcpyHostToDevice));
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+void fftpim_plan_destroy(FftpimPlan* plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->device);
+    if (plan->build_stream) cudaStreamSynchronize(plan->build_stream);
+    if (plan->fft_plan) cufftDestroy(plan->fft_plan);
+    for (void* p : plan->allocations) cudaFree(p);
+    if (plan->build_stream) cudaStreamDestroy(plan->build_stream);
+    delete plan;
+}
+
+const char* fftpim_last_error(void) { return g_last_error.c_str(); }
+
+int64_t fftpim_launch_count(void) { return (int64_t)g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// kernels.h -- host-callable launch wrappers (plan build and evaluation).
+#pragma once
+#include "plan.cuh"
+
+// Far-series parameters (pgf.py:166-462).
+struct FarSeriesParams {
+    int dim;
+    int npsp;
+    double L[3];
+    double k0_re, k0_im;
+    double ks_re[3], ks_im[3];
+    double tol;        // series_tol
+    double cutoff;     // ln(1/tol) + 8            pgf.py:56-58
+    double sep;        // 1e-13 * max(Lmax, 1)     pgf.py:93-94
+    double wood;       // 1e-8 * 2 pi / Lmax       pgf.py:88-90
+    double zmin, zmax; // extrema over the whole point set (3D lattice lead, pgf.py:394-397)
+    long long max_terms;
+    int max_layers;
+};
+
+// ---- plan build (build_kernels.cu) ----
+void launch_cell_keys(const double* pos, int64_t n, const StencilGeom& g, int* keys, DevStatus* st,
+                      cudaStream_t s);
+void launch_csr_from_sorted(const int* keys, int64_t n, int64_t ncells, int* start, cudaStream_t s);
+void launch_stencils(const double* pos, const int* perm, int64_t n, const StencilGeom& g, double* w,
+                     int* start, DevStatus* st, int where, cudaStream_t s);
+void launch_rank(const int* perm, int64_t n, int* rank, cudaStream_t s);
+void launch_embed_table(cplx* out, const int cdims[3], const int dims[3], const double h[3],
+                        const ImageSet& im, cudaStream_t s);
+void launch_count_coincident(const int dims[3], const double h[3], const ImageSet& im,
+                             unsigned long long* cnt, cudaStream_t s);
+void launch_scale(cplx* a, int64_t n, double f, cudaStream_t s);
+void launch_wrap_flags(const double* pos, int64_t n, const int code[3], const double lo[3],
+                       const double hi[3], unsigned char* flags, cudaStream_t s);
+void launch_aug_keys(const double* pos, const int* aug_orig, const unsigned char* aug_code, int64_t A,
+                     const PairGeom& pg, int* keys, cudaStream_t s);
+void launch_fill_u8(unsigned char* p, int64_t n, unsigned char v, cudaStream_t s);
+void launch_iota(int* p, int64_t n, cudaStream_t s);
+
+struct PairArgs {
+    const double* src_pos;      // original order AoS
+    const double* obs_pos;
+    const int* obs_perm;        // sorted obs -> original
+    int64_t M;
+    const int* box_start;
+    const int* box_order;
+    const int* aug_orig;
+    const unsigned char* aug_code;
+    const int* obs_start;       // sorted obs stencil starts (3 per point)
+    const double* obs_w;
+    const int* src_start;
+    const double* src_w;
+    const int* src_rank;
+    int W;                      // weights stride per axis (order+1)
+    int wdt[3];
+    // count pass
+    int64_t* counts;
+    int* d0min;                 // (27*3)
+    int* d0max;
+    unsigned long long* tallies;   // [0] self, [1] wrapped
+    // fill pass
+    const int64_t* pair_ptr;
+    const cplx* tables;
+    int* pair_src;
+    unsigned char* pair_codeid;
+    cplx* coef;
+    double* coef_r;
+    DevStatus* st;
+};
+void launch_pairs_count(const PairGeom& pg, const PairArgs& a, cudaStream_t s);
+void launch_pairs_fill(const PairGeom& pg, const ImageSet& im, const CodeTables& tabs, const PairArgs& a,
+                       cudaStream_t s);
+void launch_code_tables(const CodeTables& tabs, int ncodes, const PairGeom& pg, const ImageSet& im,
+                        cplx* tables, int64_t total, cudaStream_t s);
+void launch_far_series(const double* axes, const int kd[3], const FarSeriesParams& fp, const ImageSet& im,
+                       const GLTable& gl, cplx* out, DevStatus* st, cudaStream_t s);
+
+// ---- evaluation (eval_kernels.cu) ----
+struct EvalArgs {
+    int64_t N, M;
+    const cplx* q;              // caller order
+    cplx* u;                    // caller order
+    const int* src_perm;
+    const int* obs_perm;
+    cplx* q_sorted;
+    // near
+    StencilGeom g;
+    int cdims[3];
+    const int* cell_start;
+    const double* src_w;
+    const int* src_start;
+    const double* obs_w;
+    const int* obs_start;
+    cplx* work;
+    const cplx* khat;
+    int64_t n_fft;
+    const int64_t* pair_ptr;
+    const int* pair_src;
+    const cplx* coef;
+    const double* coef_r;
+    // far
+    StencilGeom fs, fo;
+    const double* src_fw;
+    const int* src_fstart;
+    const double* obs_fw;
+    const int* obs_fstart;
+    const cplx* far_kernel;
+    cplx* far_partial;
+    cplx* far_qg;
+    cplx* far_ug;
+    int far_blocks, far_warps;
+    int parts;
+};
+void launch_permute_q(const EvalArgs& a, cudaStream_t s);
+void launch_near_project(const EvalArgs& a, cudaStream_t s);
+void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s);
+void launch_far_project(const EvalArgs& a, cudaStream_t s);
+void launch_far_sum(const EvalArgs& a, cudaStream_t s);
+void launch_observers(const EvalArgs& a, cudaStream_t s);

@@ -1,0 +1,134 @@
+// plan.cuh -- internal plan layout and the by-value parameter blocks the
+// kernels receive.  See DESIGN.md "Data layout in HBM".
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "cmath.cuh"
+#include "../../include/fftpim.h"
+
+#define FFTPIM_MAX_IMAGES 125   // (2*i_d+1)^3 with i_d <= 2
+#define FFTPIM_MAX_ORDER 6
+#define FFTPIM_MAX_W (FFTPIM_MAX_ORDER + 1)
+
+// One uniform grid + Lagrange stencil order (grids.py:25-56, 110-140).
+struct StencilGeom {
+    int n[3];          // grid planes per axis
+    double origin[3];
+    double h[3];       // spacing (0 on a single-plane axis)
+    int order;
+    int w[3];          // stencil width per axis: order+1, or 1 on single-plane axes
+    int nc[3];         // number of distinct stencil starts per axis: n - w + 1
+    double margin[3];  // allowed extrapolation beyond the hull
+};
+
+// Image list for G_near (pgf.py:114-123).
+struct ImageSet {
+    int count;
+    double off[FFTPIM_MAX_IMAGES][3];
+    double ph_re[FFTPIM_MAX_IMAGES];
+    double ph_im[FFTPIM_MAX_IMAGES];
+    double k0_re, k0_im;
+    double sing_tol;  // near tables / direct terms (nearzone.py:213)
+    double sep_tol;   // far kernel image subtraction (pgf.py:93-94)
+};
+
+// Correction-pair discovery geometry (nearzone.py:303-364).
+struct PairGeom {
+    int dims[3];
+    double h[3];
+    double inv_h[3];
+    int nb[3];
+    int jr[3];
+    int ext[3];
+    int max_pad;
+    double r2_keep;
+    double sing_tol;
+    int same_points;
+    int ncodes;                 // distinct image codes present (<= 27)
+    signed char code[27][3];    // code vectors, index = code id
+    double shift[27][3];        // code * L
+    double phase_re[27], phase_im[27];   // exp(-j code.(kshift*L))
+};
+
+// Per-code window table of G_near(idx*h - c*L) (nearzone.py:439-451).
+struct CodeTables {
+    int64_t offset[27];
+    int lo[27][3];
+    int len[27][3];
+};
+
+// Device-side first-error record.
+struct DevStatus {
+    int code;           // FftpimStatus, 0 if none
+    int where;          // kernel-specific detail
+    long long a, b;     // indices for the message
+    int kernel_terms;
+    int pad_;
+};
+
+struct FftpimPlan {
+    FftpimProblem prob;           // copy (pointers cleared)
+    FftpimInfo info;
+    int device;
+    cudaStream_t build_stream;
+
+    // geometry
+    StencilGeom near_g, far_sg, far_og;
+    ImageSet images;
+    PairGeom pg;
+    CodeTables tabs;
+    int cdims[3];                 // circulant dims
+    int64_t n_fft;                // prod(cdims)
+    int64_t n_grid;               // prod(near dims)
+    int64_t n_far;                // far nodes
+    int far_kdims[3];             // far kernel table dims
+    bool npsp;
+
+    // points (sorted by near stencil cell)
+    int64_t N, M;
+    int* src_perm = nullptr;      // sorted -> original
+    int* src_rank = nullptr;      // original -> sorted
+    int* obs_perm = nullptr;
+    int* cell_start = nullptr;    // (ncells+1) CSR of sorted sources by near stencil start
+    double* src_w = nullptr;      // (N, 3, W) near axis weights, sorted order
+    int* src_start = nullptr;     // (N, 3) near stencil starts, sorted order
+    double* obs_w = nullptr;      // observers (aliases src_* if same_points)
+    int* obs_start = nullptr;
+    double* src_fw = nullptr;     // (N, 3, Wf) far source-grid weights
+    int* src_fstart = nullptr;
+    double* obs_fw = nullptr;     // far observer-grid weights
+    int* obs_fstart = nullptr;
+
+    // near FFT
+    cplx* khat = nullptr;         // kernel_hat / M (numpy ifftn scaling folded in)
+    cplx* work = nullptr;         // padded grid, transformed in place
+    cufftHandle fft_plan = 0;
+    cplx* q_sorted = nullptr;     // (N) charges permuted to sorted order
+
+    // corrections (CSR over sorted observers)
+    int64_t* pair_ptr = nullptr;  // (M+1)
+    int* pair_src = nullptr;      // (P) sorted source index
+    unsigned char* pair_codeid = nullptr;  // (P) code id (export only)
+    cplx* pair_coef = nullptr;    // (P) complex coefficients (dynamic / static-shifted)
+    double* pair_coef_r = nullptr;  // (P) real coefficients (NPSP)
+
+    // far
+    cplx* far_kernel = nullptr;   // (2nf-1)^3
+    cplx* far_qg = nullptr;       // projected far source grid
+    cplx* far_partial = nullptr;  // per-block partial grids
+    cplx* far_ug = nullptr;       // far observer-grid potentials
+    int far_blocks = 0;
+    int far_warps = 0;
+
+    DevStatus* status = nullptr;
+    int64_t device_bytes = 0;
+    std::vector<void*> allocations;
+};
+
+// launch-count evidence (fftpim_launch_count)
+void fftpim_count_launch(int n = 1);

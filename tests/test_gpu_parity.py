@@ -1,0 +1,159 @@
+"""CUDA path vs the reference (golden fixtures made by running it) and vs the
+CPU oracle, through the C ABI.  Bar: relative L2 <= 1e-10 in fp64 on the
+potentials (BASELINE.json north star), identical correction-pair sets."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+from cases import SMALL_CASES, case_inputs, regime_of
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def fp():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2312_02376_b200 as fp
+    fp._native.load()
+    return fp
+
+
+def ref_objects(fp, case, pos, q, obs):
+    import numpy as np
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(case["dim"]), L=case["L"], k0=case["k0"],
+                               kshift=case["kshift"], regime=fp.Regime(regime_of(case)))
+    box = fp.TargetBox(case["D"])
+    src = fp.SourcePointSet(pos, q)
+    ob = fp.ObserverPointSet(pos if obs is None else obs)
+    return cfg, box, src, ob, fp.SolverParams(**case["params"])
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_small_case_parity(fp, name):
+    case = SMALL_CASES[name]
+    g = golden(f"small_{name}.npz")
+    pos, q, obs = case_inputs(name)
+    cfg, box, src, ob, prm = ref_objects(fp, case, pos, q, obs)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = fp.build_plan(cfg, box, src, ob, prm)
+    near = plan.near
+    # identical correction-pair set, order and bookkeeping (nearzone.py:303-487)
+    assert near.pair_obs.size == int(g["n_pairs"])
+    assert digest(near.pair_obs, near.pair_src, near.pair_code) == str(g["pair_digest"])
+    assert near.n_self_pairs == int(g["n_self"]) and near.n_wrapped_pairs == int(g["n_wrap"])
+    assert near.coincident_kernel_terms == int(g["coincident_terms"])
+    assert tuple(near.grid.dims) == tuple(g["near_dims"])
+    assert tuple(near.join_radius) == tuple(g["join_radius"])
+    # coefficients
+    assert abs(near.pair_coef.sum() - complex(g["coef_sum"])) <= 1e-11 * float(g["coef_abs_sum"])
+    # far kernel table (same truncation layer by layer, pgf.py:166-195)
+    assert plan.far.kernel_terms == int(g["far_terms"])
+    assert rel_l2(plan.far.kernel, g["far_kernel"]) <= 1e-11
+    # potentials: full, near-only, far-only
+    assert rel_l2(plan.evaluate(q), g["u"]) <= TOL
+    assert rel_l2(fp.eval_near(plan.near, q), g["u_near"]) <= TOL
+    assert rel_l2(fp.eval_far(plan.far, q), g["u_far"]) <= TOL
+
+
+def _full(fp, c):
+    from paper_2312_02376_b200.workloads import CONFIGS, make_inputs
+    w = CONFIGS[c]
+    pos, q = make_inputs(c)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=w.kshift,
+                               regime=fp.Regime(w.regime))
+    plan = fp.build_plan(cfg, fp.TargetBox(w.D), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos),
+                         fp.SolverParams(**w.params()))
+    return plan, q
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_baseline_config_parity(fp, c):
+    """C1 (3D NPSP, N=4096) and C2 (1D Helmholtz, N=65536) against the reference's
+    own output on the seeded inputs."""
+    g = golden(f"c{c}_full.npz")
+    plan, q = _full(fp, c)
+    assert plan.near.pair_obs.size == int(g["n_pairs"])
+    assert digest(plan.near.pair_obs, plan.near.pair_src, plan.near.pair_code) == str(g["pair_digest"])
+    assert plan.far.kernel_terms == int(g["far_terms"])
+    assert rel_l2(plan.far.kernel, g["far_kernel"]) <= 1e-11
+    assert rel_l2(plan.evaluate(q), g["u"]) <= TOL
+
+
+def test_device_path_matches_host_and_is_deterministic(fp):
+    import torch
+    plan, q = _full(fp, 1)
+    u_host = plan.evaluate(q)
+    qd = torch.from_numpy(q).cuda()
+    u1 = plan.evaluate(qd)
+    u2 = plan.evaluate(qd)
+    torch.cuda.synchronize()
+    assert torch.equal(u1, u2)                      # fixed reduction order: bitwise repeatable
+    assert np.array_equal(u1.cpu().numpy(), u_host)
+
+
+def test_batch_and_linearity(fp):
+    plan, q = _full(fp, 2)
+    rng = np.random.default_rng(5)
+    q2 = rng.standard_normal(q.size) + 1j * rng.standard_normal(q.size)
+    ub = plan.evaluate(np.stack([q, q2, 2.0 * q - 3j * q2]))
+    assert rel_l2(ub[2], 2.0 * ub[0] - 3j * ub[1]) <= 1e-12
+    assert np.array_equal(ub[0], plan.evaluate(q))
+
+
+def test_oracle_parity_random_cases(fp):
+    """Fresh seeded instances (not in the golden set) against the CPU oracle."""
+    from oracle.pipeline import build_plan as oracle_build
+    from oracle.problem import make_problem
+    rng = np.random.default_rng(77)
+    for dim, k0, ks, D, grid, order in [
+        (3, 0, (0, 0, 0), (1, 1, 1), (8, 8, 8), 3),
+        (2, 2.0, (0.4, -0.3, 0), (1, 1, 0.6), (9, 9, 6), 2),
+        (1, 1.0 - 0.2j, (0.1, 0, 0), (1, 0.5, 0.5), (10, 6, 6), 4),
+    ]:
+        n = 180
+        pos = rng.uniform(0, 1, (n, 3)) * np.asarray(D)
+        q = rng.standard_normal(n) + 0j
+        if k0 == 0:
+            q -= q.mean()
+        else:
+            q = q + 1j * rng.standard_normal(n)
+        pb = make_problem(dim, D=D, k0=k0, kshift=ks, near_grid=grid, near_order=order, far_grid=(5, 5, 5))
+        u_ref = oracle_build(pb, pos).evaluate(q)
+        cfg = fp.PeriodicityConfig(dim=fp.Periodicity(dim), L=(1, 1, 1), k0=k0, kshift=ks,
+                                   regime=fp.Regime(pb.regime))
+        plan = fp.build_plan(cfg, fp.TargetBox(D), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos),
+                             fp.SolverParams(near_grid=grid, near_order=order, far_grid=(5, 5, 5)))
+        assert rel_l2(plan.evaluate(q), u_ref) <= TOL
+
+
+def test_errors_map_to_reference_classes(fp):
+    # a distinct source on top of an observer inside the correction region (nearzone.py:410-416)
+    pos = np.random.default_rng(3).uniform(0, 1, (50, 3))
+    obs = pos[:5].copy()
+    q = np.ones(50, dtype=complex)
+    q -= q.mean()
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity.P3D, L=(1, 1, 1))
+    with pytest.raises(fp.DomainError):
+        fp.build_plan(cfg, fp.TargetBox((1, 1, 1)), fp.SourcePointSet(pos, q), fp.ObserverPointSet(obs),
+                      fp.SolverParams(near_grid=(8, 8, 8)))
+    # exact Rayleigh-Wood anomaly: 2D, k0 = 1.5 pi, kx0 = pi/2 (hard part 5)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity.P2D, L=(1, 1, 1), k0=1.5 * np.pi,
+                               kshift=(np.pi / 2, 0, 0), regime=fp.Regime.DYNAMIC)
+    p2 = np.random.default_rng(4).uniform(0, 1, (60, 3)) * np.array([1, 1, 0.25])
+    with pytest.raises(fp.WoodAnomalyError):
+        fp.build_plan(cfg, fp.TargetBox((1, 1, 0.25)), fp.SourcePointSet(p2, np.ones(60)),
+                      fp.ObserverPointSet(p2), fp.SolverParams(near_grid=(8, 8, 4)))
