@@ -41,12 +41,11 @@ void launch_permute_q(const EvalArgs& a, cudaStream_t s) {
 template <int W>
 __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= a.n_fft) return;
-    const int c1 = a.cdims[1], c2 = a.cdims[2];
-    const int z = (int)(t % c2), y = (int)((t / c2) % c1), x = (int)(t / ((int64_t)c1 * c2));
     const StencilGeom& g = a.g;
+    if (t >= (int64_t)g.n[0] * g.n[1] * g.n[2]) return;
+    const int z = (int)(t % g.n[2]), y = (int)((t / g.n[2]) % g.n[1]), x = (int)(t / ((int64_t)g.n[1] * g.n[2]));
     cplx acc = mk(0.0);
-    if (x < g.n[0] && y < g.n[1] && z < g.n[2]) {
+    {
         const int wx = g.w[0], wy = g.w[1], wz = g.w[2];
         const int zlo = max(z - (wz - 1), 0), zhi = min(z, g.nc[2] - 1);
         for (int ia = 0; ia < wx; ++ia) {
@@ -68,12 +67,12 @@ __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
             }
         }
     }
-    a.work[t] = acc;
+    a.pad_in[((int64_t)x * a.cdims[1] + y) * a.cdims[2] + z] = acc;
 }
 
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {
     const int W = a.g.order + 1;
-    const int b = nblk(a.n_fft, 256);
+    const int b = nblk((int64_t)a.g.n[0] * a.g.n[1] * a.g.n[2], 256);
     switch (W) {
         case 2: k_near_project<2><<<b, 256, 0, s>>>(a); break;
         case 3: k_near_project<3><<<b, 256, 0, s>>>(a); break;
@@ -99,32 +98,53 @@ void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s) {
 // Each warp scatters its contiguous chunk of points into a private copy of the
 // far source grid in shared memory (lanes own distinct taps of one point, so
 // no collisions); warps are summed in order, blocks in order by k_far_reduce.
-__global__ void k_far_project(EvalArgs a) {
-    extern __shared__ cplx sgrid[];
-    const int nfx = a.fs.n[0], nfy = a.fs.n[1], nfz = a.fs.n[2];
-    const int nf = nfx * nfy * nfz;
+// Points are consumed in warp-sized batches whose stencil data is staged in
+// shared memory with one coalesced load per lane, so the per-point loop never
+// waits on global memory.
+template <int WF>
+__global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
+    extern __shared__ double smem_d[];
+    const int nfy = a.fs.n[1], nfz = a.fs.n[2];
+    const int nf = a.fs.n[0] * nfy * nfz;
     const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cplx* sgrid = reinterpret_cast<cplx*>(smem_d);
+    constexpr int REC = 3 * WF + 2;                       // weights + q per staged point
+    double* stage = smem_d + 2 * (size_t)nf * warps + warp * (32 * REC);
+    int* sstart = reinterpret_cast<int*>(smem_d + 2 * (size_t)nf * warps + warps * 32 * REC) + warp * 96;
     for (int t = threadIdx.x; t < nf * warps; t += blockDim.x) sgrid[t] = mk(0.0);
     __syncthreads();
     cplx* mine = sgrid + warp * nf;
-    const int Wf = a.fs.order + 1;
     const int wx = a.fs.w[0], wy = a.fs.w[1], wz = a.fs.w[2];
     const int taps = wx * wy * wz;
-    const int64_t gw = (int64_t)blockIdx.x * warps + warp, nw = (int64_t)gridDim.x * warps;
-    const int64_t chunk = (a.N + nw - 1) / nw;
-    const int64_t p0 = gw * chunk, p1 = min(a.N, p0 + chunk);
-    for (int64_t p = p0; p < p1; ++p) {
-        const double* w = a.src_fw + p * 3 * Wf;
-        const int* st = a.src_fstart + 3 * p;
-        const cplx qv = a.q_sorted[p];
-        for (int tp = lane; tp < taps; tp += 32) {
-            const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
-            const double wgt = (w[ia] * w[Wf + ib]) * w[2 * Wf + ic];
-            const int node = ((st[0] + ia) * nfy + (st[1] + ib)) * nfz + (st[2] + ic);
-            mine[node].re += wgt * qv.re;
-            mine[node].im += wgt * qv.im;
+    const int64_t stride = (int64_t)gridDim.x * warps * 32;
+    for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < a.N; base += stride) {
+        const int64_t p = base + lane;
+        if (p < a.N) {
+            const double* w = a.src_fw + p * 3 * WF;
+#pragma unroll
+            for (int j = 0; j < 3 * WF; ++j) stage[lane * REC + j] = w[j];
+            const cplx qv = a.q_sorted[p];
+            stage[lane * REC + 3 * WF] = qv.re;
+            stage[lane * REC + 3 * WF + 1] = qv.im;
+            sstart[lane * 3] = a.src_fstart[3 * p];
+            sstart[lane * 3 + 1] = a.src_fstart[3 * p + 1];
+            sstart[lane * 3 + 2] = a.src_fstart[3 * p + 2];
         }
         __syncwarp();
+        const int cnt = (int)min((int64_t)32, a.N - base);
+        for (int j = 0; j < cnt; ++j) {
+            const double* r = stage + j * REC;
+            const int s0 = sstart[3 * j], s1 = sstart[3 * j + 1], s2 = sstart[3 * j + 2];
+            const double qre = r[3 * WF], qim = r[3 * WF + 1];
+            for (int tp = lane; tp < taps; tp += 32) {
+                const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+                const double wgt = (r[ia] * r[WF + ib]) * r[2 * WF + ic];
+                const int node = ((s0 + ia) * nfy + (s1 + ib)) * nfz + (s2 + ic);
+                mine[node].re += wgt * qre;
+                mine[node].im += wgt * qim;
+            }
+            __syncwarp();
+        }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < nf; t += blockDim.x) {
@@ -134,51 +154,90 @@ __global__ void k_far_project(EvalArgs a) {
     }
 }
 
+// one warp per far node, fixed-order sum over the block partials
 __global__ void k_far_reduce(const cplx* __restrict__ partial, int blocks, int nf, cplx* __restrict__ qg) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (t >= nf) return;
     cplx s = mk(0.0);
-    for (int b = 0; b < blocks; ++b) s = s + partial[(int64_t)b * nf + t];
-    qg[t] = s;
+    for (int b = lane; b < blocks; b += 32) s = s + partial[(int64_t)b * nf + t];
+    s = warp_sum(s);
+    if (lane == 0) qg[t] = s;
+}
+
+size_t far_project_smem(int nf, int warps, int order) {
+    const int WF = order + 1;
+    return (size_t)nf * warps * sizeof(cplx) + (size_t)warps * 32 * (3 * WF + 2) * sizeof(double) +
+           (size_t)warps * 96 * sizeof(int);
+}
+
+template <int WF>
+static void far_project_launch(const EvalArgs& a, size_t smem, cudaStream_t s) {
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_far_project<WF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    k_far_project<WF><<<a.far_blocks, 32 * a.far_warps, smem, s>>>(a);
 }
 
 void launch_far_project(const EvalArgs& a, cudaStream_t s) {
     const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
-    const size_t smem = (size_t)nf * a.far_warps * sizeof(cplx);
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_far_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
+    const size_t smem = far_project_smem(nf, a.far_warps, a.fs.order);
+    switch (a.fs.order + 1) {
+        case 2: far_project_launch<2>(a, smem, s); break;
+        case 3: far_project_launch<3>(a, smem, s); break;
+        case 4: far_project_launch<4>(a, smem, s); break;
+        case 5: far_project_launch<5>(a, smem, s); break;
+        case 6: far_project_launch<6>(a, smem, s); break;
+        default: far_project_launch<7>(a, smem, s); break;
     }
-    k_far_project<<<a.far_blocks, 32 * a.far_warps, smem, s>>>(a);
-    k_far_reduce<<<nblk(nf, 128), 128, 0, s>>>(a.far_partial, a.far_blocks, nf, a.far_qg);
+    k_far_reduce<<<nblk((int64_t)nf * 32, 256), 256, 0, s>>>(a.far_partial, a.far_blocks, nf, a.far_qg);
     fftpim_count_launch(2);
 }
 
 // ---------------------------------------------------------------- K5b
-// ug[o] = sum_s K[o - s + (n-1)] qg[s]; one warp per observer-grid node
-__global__ void k_far_sum(EvalArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// ug[o] = sum_s K[o - s + (n-1)] qg[s].  One block per observer-grid (x, y)
+// column; the source grid is staged in shared memory, each thread sums a fixed
+// strided subset of sources for every z output, then a fixed-order block reduce.
+#define FAR_SUM_MAXZ 32
+__global__ void __launch_bounds__(256) k_far_sum(EvalArgs a) {
+    extern __shared__ cplx sq[];
     const int nx = a.fs.n[0], ny = a.fs.n[1], nz = a.fs.n[2];
     const int nf = nx * ny * nz;
-    if (o >= nf) return;
-    const int kx = 2 * nx - 1, ky = 2 * ny - 1, kz = 2 * nz - 1;
-    (void)kx;
-    const int oz = o % nz, oy = (o / nz) % ny, ox = o / (ny * nz);
-    cplx acc = mk(0.0);
-    for (int s = lane; s < nf; s += 32) {
-        const int sz = s % nz, sy = (s / nz) % ny, sx = s / (ny * nz);
-        const int idx = ((ox - sx + nx - 1) * ky + (oy - sy + ny - 1)) * kz + (oz - sz + nz - 1);
-        acc = acc + a.far_kernel[idx] * a.far_qg[s];
+    const int ky = 2 * ny - 1, kz = 2 * nz - 1;
+    const int ox = blockIdx.x / ny, oy = blockIdx.x % ny;
+    for (int t = threadIdx.x; t < nf; t += blockDim.x) sq[t] = a.far_qg[t];
+    __syncthreads();
+    cplx acc[FAR_SUM_MAXZ];
+    for (int oz = 0; oz < nz; ++oz) acc[oz] = mk(0.0);
+    const int nsc = nx * ny;   // source columns
+    for (int c = threadIdx.x; c < nsc; c += blockDim.x) {
+        const int sx = c / ny, sy = c % ny;
+        const cplx* krow = a.far_kernel + ((int64_t)(ox - sx + nx - 1) * ky + (oy - sy + ny - 1)) * kz;
+        const cplx* qcol = sq + c * nz;
+        for (int sz = 0; sz < nz; ++sz) {
+            const cplx qv = qcol[sz];
+            for (int oz = 0; oz < nz; ++oz) acc[oz] = acc[oz] + krow[oz - sz + nz - 1] * qv;
+        }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) a.far_ug[o] = acc;
+    __shared__ cplx red[8][FAR_SUM_MAXZ];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int oz = 0; oz < nz; ++oz) {
+        cplx v = warp_sum(acc[oz]);
+        if (lane == 0) red[warp][oz] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < nz) {
+        cplx v = mk(0.0);
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = v + red[w][threadIdx.x];
+        a.far_ug[(ox * ny + oy) * nz + threadIdx.x] = v;
+    }
 }
 
 void launch_far_sum(const EvalArgs& a, cudaStream_t s) {
     const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
-    k_far_sum<<<nblk((int64_t)nf * 32, 256), 256, 0, s>>>(a);
+    k_far_sum<<<a.fs.n[0] * a.fs.n[1], 256, (size_t)nf * sizeof(cplx), s>>>(a);
     fftpim_count_launch();
 }
 
@@ -205,15 +264,41 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
             acc.im += wgt * v.im;
         }
         // precorrection: u += sum coef * q[src]
+        // four pairs per lane in flight: indices and coefficients streamed with
+        // evict-first loads, then the four q gathers, then the FMAs
         const int64_t p0 = a.pair_ptr[i], p1 = a.pair_ptr[i + 1];
-        for (int64_t p = p0 + lane; p < p1; p += 32) {
-            const cplx qv = a.q_sorted[a.pair_src[p]];
+        int64_t p = p0 + lane;
+        for (; p + 96 < p1; p += 128) {
+            int src[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) src[k] = __ldcs(a.pair_src + p + 32 * k);
             if (REAL) {
-                const double c = a.coef_r[p];
+                double c[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c[k] = __ldcs(a.coef_r + p + 32 * k);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const cplx qv = a.q_sorted[src[k]];
+                    acc.re += c[k] * qv.re;
+                    acc.im += c[k] * qv.im;
+                }
+            } else {
+                double2 c[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c[k] = __ldcs(reinterpret_cast<const double2*>(a.coef + p + 32 * k));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc = acc + cplx{c[k].x, c[k].y} * a.q_sorted[src[k]];
+            }
+        }
+        for (; p < p1; p += 32) {
+            const cplx qv = a.q_sorted[__ldcs(a.pair_src + p)];
+            if (REAL) {
+                const double c = __ldcs(a.coef_r + p);
                 acc.re += c * qv.re;
                 acc.im += c * qv.im;
             } else {
-                acc = acc + a.coef[p] * qv;
+                const double2 c = __ldcs(reinterpret_cast<const double2*>(a.coef + p));
+                acc = acc + cplx{c.x, c.y} * qv;
             }
         }
     }

@@ -371,6 +371,8 @@ void build(FftpimPlan* P) {
         launch_scale(P->khat, P->n_fft, 1.0 / (double)P->n_fft, s);   // numpy ifftn's 1/M
     }
     P->work = dalloc<cplx>(P, P->n_fft);
+    P->pad_in = dalloc<cplx>(P, P->n_fft);
+    CK(cudaMemsetAsync(P->pad_in, 0, sizeof(cplx) * P->n_fft, s));   // padding stays zero: out-of-place forward FFT
     P->q_sorted = dalloc<cplx>(P, N);
 
     // ---- correction pairs (nearzone.py:245-256, 303-487)
@@ -666,9 +668,11 @@ void build(FftpimPlan* P) {
     // far evaluation scratch
     {
         const int64_t nf = P->n_far;
-        int warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (160 * 1024) / (nf * (int64_t)sizeof(cplx))));
-        if (nf * (int64_t)sizeof(cplx) > 200 * 1024) throw Fail{FFTPIM_VALUE, "far grid too large (max 12800 nodes)"};
-        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, (N + 32 * warps * 8 - 1) / (32 * warps * 8)));
+        if (nf > 3072 || fdims[2] > 32)
+            throw Fail{FFTPIM_VALUE, "far grid too large for this build (max 3072 nodes, 32 along z)"};
+        int warps = 8;
+        while (warps > 1 && far_project_smem((int)nf, warps, pr.far_order) > 200 * 1024) --warps;
+        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, (N + 32 * warps - 1) / (32 * warps)));
         P->far_warps = warps;
         P->far_blocks = blocks;
         P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
@@ -705,6 +709,7 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.obs_w = P->obs_w;
     a.obs_start = P->obs_start;
     a.work = P->work;
+    a.pad_in = P->pad_in;
     a.khat = P->khat;
     a.n_fft = P->n_fft;
     a.pair_ptr = P->pair_ptr;
@@ -747,7 +752,7 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
         if (parts & FFTPIM_NEAR) launch_near_project(a, s);
         mark(4);
         if (parts & FFTPIM_NEAR) {
-            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
             fftpim_count_launch(1);
         }
         mark(5);

@@ -92,6 +92,7 @@ struct EvalArgs {
     const double* obs_w;
     const int* obs_start;
     cplx* work;
+    cplx* pad_in;               // zero-padded FFT input; only the n^3 corner is written
     const cplx* khat;
     int64_t n_fft;
     const int64_t* pair_ptr;
@@ -115,5 +116,6 @@ void launch_permute_q(const EvalArgs& a, cudaStream_t s);
 void launch_near_project(const EvalArgs& a, cudaStream_t s);
 void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s);
 void launch_far_project(const EvalArgs& a, cudaStream_t s);
+size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);
 void launch_observers(const EvalArgs& a, cudaStream_t s);

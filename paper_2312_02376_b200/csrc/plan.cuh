@@ -106,7 +106,8 @@ struct FftpimPlan {
 
     // near FFT
     cplx* khat = nullptr;         // kernel_hat / M (numpy ifftn scaling folded in)
-    cplx* work = nullptr;         // padded grid, transformed in place
+    cplx* work = nullptr;         // spectrum / inverse-FFT buffer (in place)
+    cplx* pad_in = nullptr;       // zero-padded projection (corner written each eval)
     cufftHandle fft_plan = 0;
     cplx* q_sorted = nullptr;     // (N) charges permuted to sorted order
 
