@@ -50,13 +50,20 @@ __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
         const int zlo = max(z - (wz - 1), 0), zhi = min(z, g.nc[2] - 1);
         for (int ia = 0; ia < wx; ++ia) {
             const int sx = x - ia;
-            if (sx < 0 || sx >= g.nc[0]) continue;
-            for (int ib = 0; ib < wy; ++ib) {
+            if (sx < 0 || sx >= g.nc[0] || zlo > zhi) continue;
+            // all W candidate ranges of this x offset loaded before any point is touched
+            int r0[W], r1[W];
+#pragma unroll
+            for (int ib = 0; ib < W; ++ib) {
                 const int sy = y - ib;
-                if (sy < 0 || sy >= g.nc[1] || zlo > zhi) continue;
-                const int k0 = (sx * g.nc[1] + sy) * g.nc[2];
-                const int p0 = a.cell_start[k0 + zlo], p1 = a.cell_start[k0 + zhi + 1];
-                for (int p = p0; p < p1; ++p) {
+                const bool ok = ib < wy && sy >= 0 && sy < g.nc[1];
+                const int k0 = ok ? (sx * g.nc[1] + sy) * g.nc[2] : 0;
+                r0[ib] = ok ? a.cell_start[k0 + zlo] : 0;
+                r1[ib] = ok ? a.cell_start[k0 + zhi + 1] : 0;
+            }
+#pragma unroll
+            for (int ib = 0; ib < W; ++ib) {
+                for (int p = r0[ib]; p < r1[ib]; ++p) {
                     const double* w = a.src_w + (int64_t)p * 3 * W;
                     const int ic = z - a.src_start[3 * (int64_t)p + 2];
                     const double wgt = (w[ia] * w[W + ib]) * w[2 * W + ic];
@@ -114,8 +121,7 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
     for (int t = threadIdx.x; t < nf * warps; t += blockDim.x) sgrid[t] = mk(0.0);
     __syncthreads();
     cplx* mine = sgrid + warp * nf;
-    const int wx = a.fs.w[0], wy = a.fs.w[1], wz = a.fs.w[2];
-    const int taps = wx * wy * wz;
+    const int wfx = a.fs.w[0], wfy = a.fs.w[1], wfz = a.fs.w[2];
     const int64_t stride = (int64_t)gridDim.x * warps * 32;
     for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < a.N; base += stride) {
         const int64_t p = base + lane;
@@ -136,8 +142,12 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
             const double* r = stage + j * REC;
             const int s0 = sstart[3 * j], s1 = sstart[3 * j + 1], s2 = sstart[3 * j + 2];
             const double qre = r[3 * WF], qim = r[3 * WF + 1];
-            for (int tp = lane; tp < taps; tp += 32) {
-                const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+            // compile-time tap decomposition; taps beyond a single-plane axis are
+            // skipped (they would alias another lane's node)
+#pragma unroll
+            for (int tp = lane; tp < WF * WF * WF; tp += 32) {
+                const int ic = tp % WF, ib = (tp / WF) % WF, ia = tp / (WF * WF);
+                if (ia >= wfx || ib >= wfy || ic >= wfz) continue;
                 const double wgt = (r[ia] * r[WF + ib]) * r[2 * WF + ic];
                 const int node = ((s0 + ia) * nfy + (s1 + ib)) * nfz + (s2 + ic);
                 mine[node].re += wgt * qre;
@@ -209,28 +219,25 @@ __global__ void __launch_bounds__(256) k_far_sum(EvalArgs a) {
     const int ox = blockIdx.x / ny, oy = blockIdx.x % ny;
     for (int t = threadIdx.x; t < nf; t += blockDim.x) sq[t] = a.far_qg[t];
     __syncthreads();
-    cplx acc[FAR_SUM_MAXZ];
-    for (int oz = 0; oz < nz; ++oz) acc[oz] = mk(0.0);
+    // thread t: output oz = t % nz, source columns c = t / nz, t / nz + groups, ...
+    const int groups = blockDim.x / nz;
+    const int oz = threadIdx.x % nz, grp = threadIdx.x / nz;
+    cplx acc = mk(0.0);
     const int nsc = nx * ny;   // source columns
-    for (int c = threadIdx.x; c < nsc; c += blockDim.x) {
-        const int sx = c / ny, sy = c % ny;
-        const cplx* krow = a.far_kernel + ((int64_t)(ox - sx + nx - 1) * ky + (oy - sy + ny - 1)) * kz;
-        const cplx* qcol = sq + c * nz;
-        for (int sz = 0; sz < nz; ++sz) {
-            const cplx qv = qcol[sz];
-            for (int oz = 0; oz < nz; ++oz) acc[oz] = acc[oz] + krow[oz - sz + nz - 1] * qv;
+    if (grp < groups) {
+        for (int c = grp; c < nsc; c += groups) {
+            const int sx = c / ny, sy = c % ny;
+            const cplx* krow = a.far_kernel + ((int64_t)(ox - sx + nx - 1) * ky + (oy - sy + ny - 1)) * kz + oz + nz - 1;
+            const cplx* qcol = sq + c * nz;
+            for (int sz = 0; sz < nz; ++sz) acc = acc + krow[-sz] * qcol[sz];
         }
     }
-    __shared__ cplx red[8][FAR_SUM_MAXZ];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int oz = 0; oz < nz; ++oz) {
-        cplx v = warp_sum(acc[oz]);
-        if (lane == 0) red[warp][oz] = v;
-    }
+    __shared__ cplx red[256];
+    red[threadIdx.x] = acc;
     __syncthreads();
     if (threadIdx.x < nz) {
         cplx v = mk(0.0);
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = v + red[w][threadIdx.x];
+        for (int g = 0; g < groups; ++g) v = v + red[g * nz + threadIdx.x];
         a.far_ug[(ox * ny + oy) * nz + threadIdx.x] = v;
     }
 }
@@ -242,82 +249,105 @@ void launch_far_sum(const EvalArgs& a, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- K3 + K4 + K5c
+// One warp per G consecutive (sorted) observers.  Their correction pairs are
+// one contiguous CSR range, streamed by all 32 lanes with 8 independent loads
+// in flight per lane; each lane routes a pair to its observer's accumulator by
+// comparing against the G+1 row pointers.  Interpolation taps of the G
+// observers are spread over the lanes the same way.  Fixed lane->work mapping
+// and fixed shuffle trees make the result bitwise reproducible.
+#define OBS_G 4
+#define OBS_U 8
+template <int G>
+__device__ __forceinline__ void add_to(cplx (&acc)[G], int g, double re, double im) {
+#pragma unroll
+    for (int k = 0; k < G; ++k)
+        if (g == k) {
+            acc[k].re += re;
+            acc[k].im += im;
+        }
+}
+
 template <int W, int WF, bool REAL>
-__global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
+__global__ void __launch_bounds__(256, 3) k_observers(EvalArgs a) {
+    constexpr int G = OBS_G;
     const int lane = threadIdx.x & 31;
-    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (i >= a.M) return;
-    cplx acc = mk(0.0);
+    const int64_t i0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G;
+    if (i0 >= a.M) return;
+    const int ng = (int)min((int64_t)G, a.M - i0);
+    cplx acc[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) acc[k] = mk(0.0);
     if (a.parts & FFTPIM_NEAR) {
+        // row pointers of the G observers
+        int64_t myptr = (lane <= ng) ? a.pair_ptr[i0 + lane] : 0;
+        int64_t ptr[G + 1];
+#pragma unroll
+        for (int k = 0; k <= G; ++k) ptr[k] = __shfl_sync(0xffffffffu, myptr, min(k, ng));
         // near interpolation from the inverse-FFT buffer (top corner of the padded grid)
-        const double* w = a.obs_w + i * 3 * W;
-        const int* st = a.obs_start + 3 * i;
-        const int wx = a.g.w[0], wy = a.g.w[1], wz = a.g.w[2];
-        const int taps = wx * wy * wz;
+        // compile-time tap decomposition; single-plane axes have zero weights past
+        // the first tap and clamped indices, so their extra taps add exactly 0
+        constexpr int T3 = W * W * W;
         const int c1 = a.cdims[1], c2 = a.cdims[2];
-        for (int tp = lane; tp < taps; tp += 32) {
-            const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+        const int m0 = a.g.n[0] - 1, m1 = a.g.n[1] - 1, m2 = a.g.n[2] - 1;
+        for (int t = lane; t < ng * T3; t += 32) {
+            const int g = t / T3, tp = t - g * T3;
+            const int ic = tp % W, ib = (tp / W) % W, ia = tp / (W * W);
+            const double* w = a.obs_w + (i0 + g) * 3 * W;
+            const int* st = a.obs_start + 3 * (i0 + g);
             const double wgt = (w[ia] * w[W + ib]) * w[2 * W + ic];
-            const int64_t g = ((int64_t)(st[0] + ia) * c1 + (st[1] + ib)) * c2 + (st[2] + ic);
-            const cplx v = a.work[g];
-            acc.re += wgt * v.re;
-            acc.im += wgt * v.im;
+            const cplx v = a.work[((int64_t)min(st[0] + ia, m0) * c1 + min(st[1] + ib, m1)) * c2 + min(st[2] + ic, m2)];
+            add_to<G>(acc, g, wgt * v.re, wgt * v.im);
         }
-        // precorrection: u += sum coef * q[src]
-        // four pairs per lane in flight: indices and coefficients streamed with
-        // evict-first loads, then the four q gathers, then the FMAs
-        const int64_t p0 = a.pair_ptr[i], p1 = a.pair_ptr[i + 1];
-        int64_t p = p0 + lane;
-        for (; p + 96 < p1; p += 128) {
-            int src[4];
+        // precorrection u[m] += sum coef * q[src] over the G rows' pair range
+        for (int64_t base = ptr[0]; base < ptr[ng]; base += 32 * OBS_U) {
+            int src[OBS_U];
+            double cr[OBS_U], ci[OBS_U];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) src[k] = __ldcs(a.pair_src + p + 32 * k);
-            if (REAL) {
-                double c[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) c[k] = __ldcs(a.coef_r + p + 32 * k);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const cplx qv = a.q_sorted[src[k]];
-                    acc.re += c[k] * qv.re;
-                    acc.im += c[k] * qv.im;
+            for (int k = 0; k < OBS_U; ++k) {
+                const int64_t p = base + 32 * k + lane;
+                const bool ok = p < ptr[ng];
+                src[k] = ok ? __ldcs(a.pair_src + p) : 0;
+                if (REAL) {
+                    cr[k] = ok ? __ldcs(a.coef_r + p) : 0.0;
+                    ci[k] = 0.0;
+                } else {
+                    const double2 c = ok ? __ldcs(reinterpret_cast<const double2*>(a.coef + p)) : make_double2(0.0, 0.0);
+                    cr[k] = c.x;
+                    ci[k] = c.y;
                 }
-            } else {
-                double2 c[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) c[k] = __ldcs(reinterpret_cast<const double2*>(a.coef + p + 32 * k));
-#pragma unroll
-                for (int k = 0; k < 4; ++k) acc = acc + cplx{c[k].x, c[k].y} * a.q_sorted[src[k]];
             }
-        }
-        for (; p < p1; p += 32) {
-            const cplx qv = a.q_sorted[__ldcs(a.pair_src + p)];
-            if (REAL) {
-                const double c = __ldcs(a.coef_r + p);
-                acc.re += c * qv.re;
-                acc.im += c * qv.im;
-            } else {
-                const double2 c = __ldcs(reinterpret_cast<const double2*>(a.coef + p));
-                acc = acc + cplx{c.x, c.y} * qv;
+#pragma unroll
+            for (int k = 0; k < OBS_U; ++k) {
+                const int64_t p = base + 32 * k + lane;
+                const cplx qv = a.q_sorted[src[k]];
+                int g = 0;
+#pragma unroll
+                for (int j = 1; j < G; ++j) g += (p >= ptr[j]);
+                if (REAL)
+                    add_to<G>(acc, g, cr[k] * qv.re, cr[k] * qv.im);
+                else
+                    add_to<G>(acc, g, cr[k] * qv.re - ci[k] * qv.im, cr[k] * qv.im + ci[k] * qv.re);
             }
         }
     }
     if (a.parts & FFTPIM_FAR) {
-        const double* w = a.obs_fw + i * 3 * WF;
-        const int* st = a.obs_fstart + 3 * i;
-        const int wx = a.fo.w[0], wy = a.fo.w[1], wz = a.fo.w[2];
-        const int taps = wx * wy * wz;
-        const int ny = a.fo.n[1], nz = a.fo.n[2];
-        for (int tp = lane; tp < taps; tp += 32) {
-            const int ic = tp % wz, ib = (tp / wz) % wy, ia = tp / (wy * wz);
+        constexpr int T3 = WF * WF * WF;
+        const int nx = a.fo.n[0], ny = a.fo.n[1], nz = a.fo.n[2];
+        for (int t = lane; t < ng * T3; t += 32) {
+            const int g = t / T3, tp = t - g * T3;
+            const int ic = tp % WF, ib = (tp / WF) % WF, ia = tp / (WF * WF);
+            const double* w = a.obs_fw + (i0 + g) * 3 * WF;
+            const int* st = a.obs_fstart + 3 * (i0 + g);
             const double wgt = (w[ia] * w[WF + ib]) * w[2 * WF + ic];
-            const cplx v = a.far_ug[((st[0] + ia) * ny + (st[1] + ib)) * nz + (st[2] + ic)];
-            acc.re += wgt * v.re;
-            acc.im += wgt * v.im;
+            const cplx v = a.far_ug[(min(st[0] + ia, nx - 1) * ny + min(st[1] + ib, ny - 1)) * nz + min(st[2] + ic, nz - 1)];
+            add_to<G>(acc, g, wgt * v.re, wgt * v.im);
         }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) a.u[a.obs_perm[i]] = acc;
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+        const cplx v = warp_sum(acc[k]);
+        if (lane == k && k < ng) a.u[a.obs_perm[i0 + k]] = v;
+    }
 }
 
 template <int W, int WF>
@@ -342,7 +372,7 @@ static void obs_dispatch_far(const EvalArgs& a, int blocks, cudaStream_t s) {
 
 void launch_observers(const EvalArgs& a, cudaStream_t s) {
     if (a.M == 0) return;
-    const int blocks = nblk(a.M * 32, 256);
+    const int blocks = nblk(((a.M + OBS_G - 1) / OBS_G) * 32, 256);
     switch (a.g.order + 1) {
         case 2: obs_dispatch_far<2>(a, blocks, s); break;
         case 3: obs_dispatch_far<3>(a, blocks, s); break;
