@@ -117,7 +117,10 @@ def stage_bytes(w, info, n_far):
         "fft_forward": 2 * 16 * nfft,
         "spectrum_mul": 3 * 16 * nfft,
         "fft_inverse": 2 * 16 * nfft,
-        "observers": M * 24 + 16 * ng + P * (sc + 4) + 8 * M + 16 * N + 16 * M,
+        # K4: coefficient + int32 source index per pair, q gathered once, row sums out
+        "corr_matvec": P * (sc + 4) + 16 * N + 16 * M,
+        # K3 + K5c + fix-up: observer stencil, grid reads, row sums, u written once
+        "observers": M * 24 + 16 * ng + 8 * M + 16 * M + 16 * M,
     }
 
 

@@ -135,11 +135,11 @@ FFTPIM_API void fftpim_plan_destroy(FftpimPlan* plan);
 FFTPIM_API const char* fftpim_last_error(void);
 
 /* One evaluation (batch 1, device pointers) with CUDA events recorded on
- * `stream` between the stages; stage_ms[0..7] receives the device time of
+ * `stream` between the stages; stage_ms[0..8] receives the device time of
  *   0 permute q  1 far projection  2 far grid sum  3 near projection
- *   4 forward FFT  5 spectrum multiply  6 inverse FFT  7 observer pass
+ *   4 forward FFT  5 spectrum multiply  6 inverse FFT  7 correction matvec  8 observer pass
  * (interpolation + precorrection + far interpolation).  Diagnostic only. */
-#define FFTPIM_N_STAGES 8
+#define FFTPIM_N_STAGES 9
 FFTPIM_API int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t parts,
                                    void* stream, double* stage_ms);
 

@@ -12,7 +12,8 @@ import os
 from .exceptions import (DomainError, KernelCacheError, NativeLibraryError, NotConvergedError,
                          PerisumError, SeparationError, WoodAnomalyError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfftpim.so")
+LIB_PATH = os.environ.get("FFTPIM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                          "libfftpim.so")
 
 OK, VALIDATION, DOMAIN, WOOD, NOT_CONVERGED, SEPARATION, KERNEL_CACHE, CUDA, VALUE = range(9)
 NEAR, FAR, ALL = 1, 2, 3
@@ -48,9 +49,9 @@ class Info(C.Structure):
 EXPORTED = ("fftpim_plan_create", "fftpim_plan_evaluate", "fftpim_plan_evaluate_host",
             "fftpim_plan_info", "fftpim_plan_export", "fftpim_plan_set_far_kernel",
             "fftpim_plan_destroy", "fftpim_last_error", "fftpim_launch_count", "fftpim_plan_profile")
-N_STAGES = 8
+N_STAGES = 9
 STAGES = ("permute_q", "far_project", "far_sum", "near_project", "fft_forward", "spectrum_mul",
-          "fft_inverse", "observers")
+          "fft_inverse", "corr_matvec", "observers")
 
 _lib = None
 _load_error = None

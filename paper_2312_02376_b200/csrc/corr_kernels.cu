@@ -1,0 +1,303 @@
+// corr_kernels.cu -- the correction matvec (K4, nearzone.py:506-524) and the
+// fused observer pass (K3 near interpolation grids.py:183-188 + K5c far
+// interpolation farzone.py:159 + the K4 row fix-up).
+//
+// K4 streams the pair list flat, one warp per CORR_TILE (=256) consecutive
+// pairs, independent of the row (observer) structure:
+//   1. coalesced strided loads of the int32 source indices, the coefficients and
+//      the tile's row-start bits (1 bit per pair, set where an observer's pairs
+//      begin) -- all independent, one memory round trip;
+//   2. the q gathers and products (second round trip, L2-resident q);
+//   3. a shared-memory transpose to 8 consecutive pairs per lane, a lane-local
+//      segmented sum and a 5-step warp segmented scan for the carries;
+//   4. every (row, tile) segment total goes to seg_val[seg_base[tile] + k].
+// The observer pass adds the <= 1 + P/M/256 segments of its row in order.
+// No atomics, fixed orders: bitwise reproducible.
+#include <cub/device/device_scan.cuh>
+
+#include "geom.cuh"
+#include "kernels.h"
+
+static inline int nblk64(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+__device__ __forceinline__ cplx wsum(cplx v) {
+    for (int o = 16; o > 0; o >>= 1) {
+        v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
+        v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
+    }
+    return v;
+}
+
+// ------------------------------------------------------------- plan-build metadata
+__global__ void k_head_bits(const int64_t* __restrict__ ptr, int64_t M, unsigned* bits) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int64_t p = ptr[i];
+    if (p < ptr[i + 1]) atomicOr(bits + (p >> 5), 1u << (p & 31));
+}
+
+__global__ void k_row_spans(const int64_t* __restrict__ ptr, int64_t M, int64_t* spans) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > M) return;
+    if (i == M) {
+        spans[i] = 0;
+        return;
+    }
+    const int64_t p0 = ptr[i], p1 = ptr[i + 1];
+    spans[i] = p0 == p1 ? 0 : (p1 - 1) / CORR_TILE - p0 / CORR_TILE + 1;
+}
+
+// global index of the segment holding the first pair of tile t
+__global__ void k_seg_base(const int64_t* __restrict__ ptr, const int64_t* __restrict__ seg_first, int64_t M,
+                           int64_t T, int64_t* seg_base) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int64_t p = t * CORR_TILE;
+    int64_t lo = 0, hi = M;   // last row with ptr[row] <= p (ptr[lo] <= p < ptr[hi])
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ptr[mid] <= p) lo = mid; else hi = mid;
+    }
+    seg_base[t] = seg_first[lo] + (t - ptr[lo] / CORR_TILE);
+}
+
+void build_corr_metadata(const int64_t* ptr, int64_t M, int64_t P, int64_t T, unsigned* bits, int64_t* seg_first,
+                         int64_t* seg_base, int64_t* spans_tmp, int64_t* n_segments, cudaStream_t s) {
+    cudaMemsetAsync(bits, 0, sizeof(unsigned) * ((P + 31) / 32 + 8), s);
+    if (M > 0) k_head_bits<<<nblk64(M, 256), 256, 0, s>>>(ptr, M, bits);
+    k_row_spans<<<nblk64(M + 1, 256), 256, 0, s>>>(ptr, M, spans_tmp);
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, spans_tmp, seg_first, (int)(M + 1), s);
+    void* tmp = nullptr;
+    cudaMallocAsync(&tmp, bytes + 16, s);
+    cub::DeviceScan::ExclusiveSum(tmp, bytes, spans_tmp, seg_first, (int)(M + 1), s);
+    cudaFreeAsync(tmp, s);
+    if (T > 0) k_seg_base<<<nblk64(T, 256), 256, 0, s>>>(ptr, seg_first, M, T, seg_base);
+    cudaMemcpyAsync(n_segments, seg_first + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fftpim_count_launch(5);
+}
+
+// ------------------------------------------------------------- K4 warp tiles
+// Tile = 8 groups of 32 consecutive pairs (pair e = 32k + lane), loaded
+// coalesced.  Each lane keeps a running partial of the current (row, tile)
+// segment; a group without a row start (the common case: ~221 pairs per row at
+// C2, ~13k at C3) costs nothing beyond the FMAs.  A group containing row
+// starts closes segments with one fixed-tree warp sum per start.
+#ifndef CORR_WARPS
+#define CORR_WARPS 8
+#endif
+#ifndef CORR_MINB
+#define CORR_MINB 3
+#endif
+template <bool REAL>
+__global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
+    for (int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp; t < T; t += (int64_t)gridDim.x * CORR_WARPS) {
+        const int64_t T0 = t * CORR_TILE;
+        const int valid = (int)min((int64_t)CORR_TILE, a.n_pairs - T0);
+        // 1. independent loads: indices, coefficients, row-start words, segment base
+        int src[8];
+        double cr[8], ci[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int e = 32 * k + lane;
+            const bool ok = e < valid;
+            src[k] = ok ? __ldcs(a.pair_src + T0 + e) : 0;
+            if (REAL) {
+                cr[k] = ok ? __ldcs(a.coef_r + T0 + e) : 0.0;
+                ci[k] = 0.0;
+            } else {
+                const double2 c = ok ? __ldcs(reinterpret_cast<const double2*>(a.coef) + T0 + e) : make_double2(0.0, 0.0);
+                cr[k] = c.x;
+                ci[k] = c.y;
+            }
+        }
+        // row-start words of the 8 groups: lane k < 8 loads word k, then broadcast per group
+        const unsigned myword = lane < 8 ? a.head_bits[(T0 >> 5) + lane] : 0u;
+        const int64_t sbase = a.seg_base[t];
+        // 2. gathers (all 8 in flight)
+        double qr[8], qi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#ifdef CORR_NOGATHER   // diagnostic variant: stream-only cost of K4
+            const cplx qv = a.q_sorted[(src[k] & 31) + lane];
+#else
+            const cplx qv = a.q_sorted[src[k]];
+#endif
+            qr[k] = qv.re;
+            qi[k] = qv.im;
+        }
+        // 3. segmented accumulation in pair order
+        double accr = 0.0, acci = 0.0;
+        int seg = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double pr = cr[k] * qr[k] - ci[k] * qi[k];
+            const double pi = cr[k] * qi[k] + ci[k] * qr[k];
+            unsigned f = __shfl_sync(0xffffffffu, myword, k);
+            if (k == 0) f &= ~1u;   // a row starting at the tile start is segment 0 itself
+            if (f == 0u) {
+                accr += pr;
+                acci += pi;
+                continue;
+            }
+            // close the open segment with the lanes before the first start
+            int s = __ffs(f) - 1;
+            {
+                double vr = accr + (lane < s ? pr : 0.0), vi = acci + (lane < s ? pi : 0.0);
+                const cplx v = wsum(cplx{vr, vi});
+                if (lane == 0) a.seg_val[sbase + seg] = v;
+                ++seg;
+            }
+            f &= f - 1u;
+            // segments wholly inside this group
+            while (f) {
+                const int s2 = __ffs(f) - 1;
+                const bool in = lane >= s && lane < s2;
+                const cplx v = wsum(cplx{in ? pr : 0.0, in ? pi : 0.0});
+                if (lane == 0) a.seg_val[sbase + seg] = v;
+                ++seg;
+                s = s2;
+                f &= f - 1u;
+            }
+            // the last start opens the new running segment
+            accr = lane >= s ? pr : 0.0;
+            acci = lane >= s ? pi : 0.0;
+        }
+        const cplx v = wsum(cplx{accr, acci});
+        if (lane == 0) a.seg_val[sbase + seg] = v;
+    }
+}
+
+void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
+    if (a.n_pairs == 0) return;
+    const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
+    const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, 148 * CORR_MINB);
+    if (a.coef_r)
+        k_corr_tiles<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+    else
+        k_corr_tiles<false><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+    fftpim_count_launch();
+}
+
+// ------------------------------------------------------------- K3 + K5c + fix-up
+// Four lanes per observer (lane sub handles x-offsets ia = sub, sub+4, ...);
+// each walks its (ia, ib) rows of the stencil with the z taps contiguous in
+// memory.  The far observer grid (<= 48 KB) is staged in shared memory.  The
+// quad is reduced with two fixed xor-shuffles, then lane 0 adds the observer's
+// K4 segments.  Single-plane axes: weights past the first tap are zero and the
+// indices are clamped, so those taps add exactly 0.
+#define OBS_LPO 4
+__device__ __forceinline__ cplx corr_of_row(const EvalArgs& a, int64_t i) {
+    const int64_t p0 = a.pair_ptr[i], p1 = a.pair_ptr[i + 1];
+    if (p0 == p1) return mk(0.0);
+    const int64_t span = (p1 - 1) / CORR_TILE - p0 / CORR_TILE + 1;
+    const cplx* sv = a.seg_val + a.seg_first[i];
+    cplx s = sv[0];
+    for (int64_t j = 1; j < span; ++j) s = s + sv[j];
+    return s;
+}
+
+template <int W, int WF>
+__global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
+    extern __shared__ cplx sfar[];
+    const int nfx = a.fo.n[0], nfy = a.fo.n[1], nfz = a.fo.n[2];
+    if (a.parts & FFTPIM_FAR) {
+        for (int t = threadIdx.x; t < nfx * nfy * nfz; t += blockDim.x) sfar[t] = a.far_ug[t];
+        __syncthreads();
+    }
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i = gt / OBS_LPO;
+    const int sub = (int)(gt % OBS_LPO);
+    const bool active = i < a.M;
+    const int64_t ii = active ? i : a.M - 1;
+    double ar = 0.0, ai = 0.0;
+    if (a.parts & FFTPIM_NEAR) {
+        const double* w = a.obs_w + ii * 3 * W;
+        const int* st = a.obs_start + 3 * ii;
+        const int c1 = a.cdims[1], c2 = a.cdims[2];
+        const int m0 = a.g.n[0] - 1, m1 = a.g.n[1] - 1, m2 = a.g.n[2] - 1;
+        const int s0 = st[0], s1 = st[1], s2 = st[2];
+        double wz[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) wz[c] = w[2 * W + c];
+        for (int ia = sub; ia < W; ia += OBS_LPO) {
+            const double wx = w[ia];
+            const int64_t xo = (int64_t)min(s0 + ia, m0) * c1;
+#pragma unroll
+            for (int ib = 0; ib < W; ++ib) {
+                const double wxy = wx * w[W + ib];
+                const cplx* row = a.work + (xo + min(s1 + ib, m1)) * c2;
+#pragma unroll
+                for (int ic = 0; ic < W; ++ic) {
+                    const cplx v = row[min(s2 + ic, m2)];
+                    const double wgt = wxy * wz[ic];
+                    ar += wgt * v.re;
+                    ai += wgt * v.im;
+                }
+            }
+        }
+    }
+    if (a.parts & FFTPIM_FAR) {
+        const double* w = a.obs_fw + ii * 3 * WF;
+        const int* st = a.obs_fstart + 3 * ii;
+        const int s0 = st[0], s1 = st[1], s2 = st[2];
+        double wz[WF];
+#pragma unroll
+        for (int c = 0; c < WF; ++c) wz[c] = w[2 * WF + c];
+        for (int ia = sub; ia < WF; ia += OBS_LPO) {
+            const double wx = w[ia];
+            const int xo = min(s0 + ia, nfx - 1) * nfy;
+#pragma unroll
+            for (int ib = 0; ib < WF; ++ib) {
+                const double wxy = wx * w[WF + ib];
+                const cplx* row = sfar + (xo + min(s1 + ib, nfy - 1)) * nfz;
+#pragma unroll
+                for (int ic = 0; ic < WF; ++ic) {
+                    const cplx v = row[min(s2 + ic, nfz - 1)];
+                    const double wgt = wxy * wz[ic];
+                    ar += wgt * v.re;
+                    ai += wgt * v.im;
+                }
+            }
+        }
+    }
+    ar += __shfl_xor_sync(0xffffffffu, ar, 1);
+    ai += __shfl_xor_sync(0xffffffffu, ai, 1);
+    ar += __shfl_xor_sync(0xffffffffu, ar, 2);
+    ai += __shfl_xor_sync(0xffffffffu, ai, 2);
+    if (active && sub == 0) {
+        cplx v{ar, ai};
+        if (a.parts & FFTPIM_NEAR) v = v + corr_of_row(a, i);
+        a.u[a.obs_perm[i]] = v;
+    }
+}
+
+template <int W>
+static void obs_dispatch_far(const EvalArgs& a, int blocks, size_t smem, cudaStream_t s) {
+    switch (a.fo.order + 1) {
+        case 2: k_observers<W, 2><<<blocks, 256, smem, s>>>(a); break;
+        case 3: k_observers<W, 3><<<blocks, 256, smem, s>>>(a); break;
+        case 4: k_observers<W, 4><<<blocks, 256, smem, s>>>(a); break;
+        case 5: k_observers<W, 5><<<blocks, 256, smem, s>>>(a); break;
+        case 6: k_observers<W, 6><<<blocks, 256, smem, s>>>(a); break;
+        default: k_observers<W, 7><<<blocks, 256, smem, s>>>(a); break;
+    }
+}
+
+void launch_observers(const EvalArgs& a, cudaStream_t s) {
+    if (a.M == 0) return;
+    const int blocks = nblk64(a.M * OBS_LPO, 256);
+    const size_t smem = (a.parts & FFTPIM_FAR) ? (size_t)a.fo.n[0] * a.fo.n[1] * a.fo.n[2] * sizeof(cplx) : 0;
+    switch (a.g.order + 1) {
+        case 2: obs_dispatch_far<2>(a, blocks, smem, s); break;
+        case 3: obs_dispatch_far<3>(a, blocks, smem, s); break;
+        case 4: obs_dispatch_far<4>(a, blocks, smem, s); break;
+        case 5: obs_dispatch_far<5>(a, blocks, smem, s); break;
+        case 6: obs_dispatch_far<6>(a, blocks, smem, s); break;
+        default: obs_dispatch_far<7>(a, blocks, smem, s); break;
+    }
+    fftpim_count_launch();
+}

@@ -248,138 +248,3 @@ void launch_far_sum(const EvalArgs& a, cudaStream_t s) {
     fftpim_count_launch();
 }
 
-// ---------------------------------------------------------------- K3 + K4 + K5c
-// One warp per G consecutive (sorted) observers.  Their correction pairs are
-// one contiguous CSR range, streamed by all 32 lanes with 8 independent loads
-// in flight per lane; each lane routes a pair to its observer's accumulator by
-// comparing against the G+1 row pointers.  Interpolation taps of the G
-// observers are spread over the lanes the same way.  Fixed lane->work mapping
-// and fixed shuffle trees make the result bitwise reproducible.
-#define OBS_G 4
-#define OBS_U 8
-template <int G>
-__device__ __forceinline__ void add_to(cplx (&acc)[G], int g, double re, double im) {
-#pragma unroll
-    for (int k = 0; k < G; ++k)
-        if (g == k) {
-            acc[k].re += re;
-            acc[k].im += im;
-        }
-}
-
-template <int W, int WF, bool REAL>
-__global__ void __launch_bounds__(256, 3) k_observers(EvalArgs a) {
-    constexpr int G = OBS_G;
-    const int lane = threadIdx.x & 31;
-    const int64_t i0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G;
-    if (i0 >= a.M) return;
-    const int ng = (int)min((int64_t)G, a.M - i0);
-    cplx acc[G];
-#pragma unroll
-    for (int k = 0; k < G; ++k) acc[k] = mk(0.0);
-    if (a.parts & FFTPIM_NEAR) {
-        // row pointers of the G observers
-        int64_t myptr = (lane <= ng) ? a.pair_ptr[i0 + lane] : 0;
-        int64_t ptr[G + 1];
-#pragma unroll
-        for (int k = 0; k <= G; ++k) ptr[k] = __shfl_sync(0xffffffffu, myptr, min(k, ng));
-        // near interpolation from the inverse-FFT buffer (top corner of the padded grid)
-        // compile-time tap decomposition; single-plane axes have zero weights past
-        // the first tap and clamped indices, so their extra taps add exactly 0
-        constexpr int T3 = W * W * W;
-        const int c1 = a.cdims[1], c2 = a.cdims[2];
-        const int m0 = a.g.n[0] - 1, m1 = a.g.n[1] - 1, m2 = a.g.n[2] - 1;
-        for (int t = lane; t < ng * T3; t += 32) {
-            const int g = t / T3, tp = t - g * T3;
-            const int ic = tp % W, ib = (tp / W) % W, ia = tp / (W * W);
-            const double* w = a.obs_w + (i0 + g) * 3 * W;
-            const int* st = a.obs_start + 3 * (i0 + g);
-            const double wgt = (w[ia] * w[W + ib]) * w[2 * W + ic];
-            const cplx v = a.work[((int64_t)min(st[0] + ia, m0) * c1 + min(st[1] + ib, m1)) * c2 + min(st[2] + ic, m2)];
-            add_to<G>(acc, g, wgt * v.re, wgt * v.im);
-        }
-        // precorrection u[m] += sum coef * q[src] over the G rows' pair range
-        for (int64_t base = ptr[0]; base < ptr[ng]; base += 32 * OBS_U) {
-            int src[OBS_U];
-            double cr[OBS_U], ci[OBS_U];
-#pragma unroll
-            for (int k = 0; k < OBS_U; ++k) {
-                const int64_t p = base + 32 * k + lane;
-                const bool ok = p < ptr[ng];
-                src[k] = ok ? __ldcs(a.pair_src + p) : 0;
-                if (REAL) {
-                    cr[k] = ok ? __ldcs(a.coef_r + p) : 0.0;
-                    ci[k] = 0.0;
-                } else {
-                    const double2 c = ok ? __ldcs(reinterpret_cast<const double2*>(a.coef + p)) : make_double2(0.0, 0.0);
-                    cr[k] = c.x;
-                    ci[k] = c.y;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < OBS_U; ++k) {
-                const int64_t p = base + 32 * k + lane;
-                const cplx qv = a.q_sorted[src[k]];
-                int g = 0;
-#pragma unroll
-                for (int j = 1; j < G; ++j) g += (p >= ptr[j]);
-                if (REAL)
-                    add_to<G>(acc, g, cr[k] * qv.re, cr[k] * qv.im);
-                else
-                    add_to<G>(acc, g, cr[k] * qv.re - ci[k] * qv.im, cr[k] * qv.im + ci[k] * qv.re);
-            }
-        }
-    }
-    if (a.parts & FFTPIM_FAR) {
-        constexpr int T3 = WF * WF * WF;
-        const int nx = a.fo.n[0], ny = a.fo.n[1], nz = a.fo.n[2];
-        for (int t = lane; t < ng * T3; t += 32) {
-            const int g = t / T3, tp = t - g * T3;
-            const int ic = tp % WF, ib = (tp / WF) % WF, ia = tp / (WF * WF);
-            const double* w = a.obs_fw + (i0 + g) * 3 * WF;
-            const int* st = a.obs_fstart + 3 * (i0 + g);
-            const double wgt = (w[ia] * w[WF + ib]) * w[2 * WF + ic];
-            const cplx v = a.far_ug[(min(st[0] + ia, nx - 1) * ny + min(st[1] + ib, ny - 1)) * nz + min(st[2] + ic, nz - 1)];
-            add_to<G>(acc, g, wgt * v.re, wgt * v.im);
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-        const cplx v = warp_sum(acc[k]);
-        if (lane == k && k < ng) a.u[a.obs_perm[i0 + k]] = v;
-    }
-}
-
-template <int W, int WF>
-static void obs_dispatch_real(const EvalArgs& a, int blocks, cudaStream_t s) {
-    if (a.coef_r)
-        k_observers<W, WF, true><<<blocks, 256, 0, s>>>(a);
-    else
-        k_observers<W, WF, false><<<blocks, 256, 0, s>>>(a);
-}
-
-template <int W>
-static void obs_dispatch_far(const EvalArgs& a, int blocks, cudaStream_t s) {
-    switch (a.fo.order + 1) {
-        case 2: obs_dispatch_real<W, 2>(a, blocks, s); break;
-        case 3: obs_dispatch_real<W, 3>(a, blocks, s); break;
-        case 4: obs_dispatch_real<W, 4>(a, blocks, s); break;
-        case 5: obs_dispatch_real<W, 5>(a, blocks, s); break;
-        case 6: obs_dispatch_real<W, 6>(a, blocks, s); break;
-        default: obs_dispatch_real<W, 7>(a, blocks, s); break;
-    }
-}
-
-void launch_observers(const EvalArgs& a, cudaStream_t s) {
-    if (a.M == 0) return;
-    const int blocks = nblk(((a.M + OBS_G - 1) / OBS_G) * 32, 256);
-    switch (a.g.order + 1) {
-        case 2: obs_dispatch_far<2>(a, blocks, s); break;
-        case 3: obs_dispatch_far<3>(a, blocks, s); break;
-        case 4: obs_dispatch_far<4>(a, blocks, s); break;
-        case 5: obs_dispatch_far<5>(a, blocks, s); break;
-        case 6: obs_dispatch_far<6>(a, blocks, s); break;
-        default: obs_dispatch_far<7>(a, blocks, s); break;
-    }
-    fftpim_count_launch();
-}

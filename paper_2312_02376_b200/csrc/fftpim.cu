@@ -605,6 +605,17 @@ void build(FftpimPlan* P) {
     pa.coef = P->pair_coef;
     pa.coef_r = P->pair_coef_r;
     launch_pairs_fill(pg, im, tb, pa, s);
+    P->n_tiles = (npairs + CORR_TILE - 1) / CORR_TILE;
+    P->head_bits = dalloc<unsigned>(P, (npairs + 31) / 32 + 8);
+    P->seg_first = dalloc<int64_t>(P, M + 1);
+    P->seg_base = dalloc<int64_t>(P, P->n_tiles);
+    {
+        int64_t* spans = dalloc<int64_t>(P, M + 1);
+        build_corr_metadata(P->pair_ptr, M, npairs, P->n_tiles, P->head_bits, P->seg_first, P->seg_base, spans,
+                            &P->n_segments, s);
+        dfree(P, spans);
+    }
+    P->seg_val = dalloc<cplx>(P, P->n_segments);
     check_status(P, "correction coefficients");
     CK(cudaStreamSynchronize(s));
     dfree(P, tables);
@@ -716,6 +727,11 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.pair_src = P->pair_src;
     a.coef = P->pair_coef;
     a.coef_r = P->pair_coef_r;
+    a.n_pairs = P->info.n_pairs;
+    a.head_bits = P->head_bits;
+    a.seg_base = P->seg_base;
+    a.seg_first = P->seg_first;
+    a.seg_val = P->seg_val;
     a.fs = P->far_sg;
     a.fo = P->far_og;
     a.src_fw = P->src_fw;
@@ -763,8 +779,10 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
             fftpim_count_launch(1);
         }
         mark(7);
-        launch_observers(a, s);
+        if (parts & FFTPIM_NEAR) launch_corr_tiles(a, s);
         mark(8);
+        launch_observers(a, s);
+        mark(9);
     }
     CK(cudaGetLastError());
 }

@@ -99,6 +99,11 @@ struct EvalArgs {
     const int* pair_src;
     const cplx* coef;
     const double* coef_r;
+    int64_t n_pairs;
+    const unsigned* head_bits;  // bit p set where an observer's pair range starts
+    const int64_t* seg_base;    // per CORR_TILE tile: global index of its first segment
+    const int64_t* seg_first;   // per observer: global index of its first segment
+    cplx* seg_val;              // (row, tile) segment sums
     // far
     StencilGeom fs, fo;
     const double* src_fw;
@@ -119,3 +124,9 @@ void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);
 void launch_observers(const EvalArgs& a, cudaStream_t s);
+
+// ---- correction matvec (corr_kernels.cu)
+#define CORR_TILE 256
+void build_corr_metadata(const int64_t* ptr, int64_t M, int64_t P, int64_t T, unsigned* bits, int64_t* seg_first,
+                         int64_t* seg_base, int64_t* spans_tmp, int64_t* n_segments, cudaStream_t s);
+void launch_corr_tiles(const EvalArgs& a, cudaStream_t s);

@@ -117,6 +117,12 @@ struct FftpimPlan {
     unsigned char* pair_codeid = nullptr;  // (P) code id (export only)
     cplx* pair_coef = nullptr;    // (P) complex coefficients (dynamic / static-shifted)
     double* pair_coef_r = nullptr;  // (P) real coefficients (NPSP)
+    int64_t n_tiles = 0;          // CORR_TILE-pair tiles of the correction stream
+    int64_t n_segments = 0;       // (observer, tile) segments
+    unsigned* head_bits = nullptr;
+    int64_t* seg_base = nullptr;
+    int64_t* seg_first = nullptr;
+    cplx* seg_val = nullptr;
 
     // far
     cplx* far_kernel = nullptr;   // (2nf-1)^3
