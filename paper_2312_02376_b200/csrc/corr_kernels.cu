@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
     if (a.parts & FFTPIM_NEAR) {
         const double* w = a.obs_w + ii * 3 * W;
         const int* st = a.obs_start + 3 * ii;
-        const int c1 = a.cdims[1], c2 = a.cdims[2];
+        const int c1 = a.gi1, c2 = a.gi2;
         const int m0 = a.g.n[0] - 1, m1 = a.g.n[1] - 1, m2 = a.g.n[2] - 1;
         const int s0 = st[0], s1 = st[1], s2 = st[2];
         double wz[W];
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
 #pragma unroll
             for (int ib = 0; ib < W; ++ib) {
                 const double wxy = wx * w[W + ib];
-                const cplx* row = a.work + (xo + min(s1 + ib, m1)) * c2;
+                const cplx* row = a.interp_grid + (xo + min(s1 + ib, m1)) * c2;
 #pragma unroll
                 for (int ic = 0; ic < W; ++ic) {
                     const cplx v = row[min(s2 + ic, m2)];

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
             }
         }
     }
-    a.pad_in[((int64_t)x * a.cdims[1] + y) * a.cdims[2] + z] = acc;
+    a.k1_out[((int64_t)x * a.go1 + y) * a.go2 + z] = acc;
 }
 
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {

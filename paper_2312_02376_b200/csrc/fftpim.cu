@@ -210,6 +210,116 @@ void sort_points(FftpimPlan* P, const double* d_pos, int64_t n, int* perm, int* 
     CK(cudaFreeAsync(iota, s));
 }
 
+// Radix factorisation for the Stockham stages: 4s, a 2, then small primes.
+bool fft_radices(int L, int* radix, int* nrad) {
+    int n = 0;
+    while (L % 4 == 0 && n < 24) radix[n++] = 4, L /= 4;
+    while (L % 2 == 0 && n < 24) radix[n++] = 2, L /= 2;
+    for (int p = 3; p <= 31 && L > 1; p += 2)
+        while (L % p == 0 && n < 24) radix[n++] = p, L /= p;
+    *nrad = n;
+    return L == 1;
+}
+
+// Pruned column-FFT pipeline for the zero-padded convolution (fft_kernels.cu).
+// Falls back to cuFFT full transforms when a doubled axis has a prime factor > 31
+// or is longer than 2048.
+void setup_fft_pipeline(FftpimPlan* P, const int dims[3], cudaStream_t s) {
+    const int n0 = dims[0], n1 = dims[1], n2 = dims[2];
+    const int L[3] = {P->cdims[0], P->cdims[1], P->cdims[2]};
+    int rad[3][24], nr[3];
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] == 1) continue;
+        if (L[a] > 2048 || !fft_radices(L[a], rad[a], &nr[a])) return;
+    }
+    P->custom_fft = true;
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] == 1) continue;
+        std::vector<cplx> tw(L[a]);
+        for (int t = 0; t < L[a]; ++t) {
+            long double ang = 2.0L * 3.141592653589793238462643383279502884L * t / L[a];
+            tw[t] = cplx{(double)cosl(ang), (double)-sinl(ang)};
+        }
+        P->twiddle[a] = dalloc<cplx>(P, L[a]);
+        CK(cudaMemcpyAsync(P->twiddle[a], tw.data(), sizeof(cplx) * L[a], cudaMemcpyHostToDevice, s));
+        // per-pass compact twiddles: pass (r, p): exp(-2 pi i q k / (p r)), q = 1..r-1, k < p
+        std::vector<cplx> twp;
+        int p = 1;
+        for (int ri = 0; ri < nr[a]; ++ri) {
+            const int r = rad[a][ri];
+            for (int q = 1; q < r; ++q)
+                for (int k = 0; k < p; ++k) twp.push_back(tw[(int64_t)q * k * (L[a] / (p * r)) % L[a]]);
+            p *= r;
+        }
+        P->n_twiddle_pass[a] = (int)twp.size();
+        P->twiddle_pass[a] = dalloc<cplx>(P, std::max<int64_t>(1, (int64_t)twp.size()));
+        if (!twp.empty())
+            CK(cudaMemcpyAsync(P->twiddle_pass[a], twp.data(), sizeof(cplx) * twp.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    P->qg = dalloc<cplx>(P, (int64_t)n0 * n1 * n2);
+    cplx* A = P->qg;
+    if (n2 > 1) A = P->fbufA = dalloc<cplx>(P, (int64_t)n0 * n1 * L[2]);
+    cplx* Bb = A;
+    if (n1 > 1) Bb = P->fbufB = dalloc<cplx>(P, (int64_t)n0 * L[1] * L[2]);
+    auto base = [&](int axis, int sign) {
+        FftStage st{};
+        st.L = L[axis];
+        st.nrad = nr[axis];
+        for (int k = 0; k < nr[axis]; ++k) st.radix[k] = rad[axis][k];
+        st.tw = P->twiddle[axis];
+        st.twp = P->twiddle_pass[axis];
+        st.ntwp = P->n_twiddle_pass[axis];
+        st.sign = sign;
+        return st;
+    };
+    const int64_t L12 = (int64_t)L[1] * L[2];
+    if (n2 > 1) {   // S1: z forward, qg -> A
+        FftStage st = base(2, -1);
+        st.in = P->qg; st.out = A; st.lin = n2; st.lout = L[2]; st.in_stride = 1; st.out_stride = 1;
+        st.nb0 = n1; st.in_s0 = n2; st.out_s0 = L[2];
+        st.nb1 = n0; st.in_s1 = (int64_t)n1 * n2; st.out_s1 = (int64_t)n1 * L[2];
+        P->stage[0] = st;
+        P->stage_on[0] = true;
+        // S5: z inverse, A -> qg
+        FftStage t = base(2, +1);
+        t.in = A; t.out = P->qg; t.lin = L[2]; t.lout = n2; t.in_stride = 1; t.out_stride = 1;
+        t.nb0 = n1; t.in_s0 = L[2]; t.out_s0 = n2;
+        t.nb1 = n0; t.in_s1 = (int64_t)n1 * L[2]; t.out_s1 = (int64_t)n1 * n2;
+        P->stage[4] = t;
+        P->stage_on[4] = true;
+    }
+    if (n1 > 1) {   // S2: y forward, A -> B
+        FftStage st = base(1, -1);
+        st.in = A; st.out = Bb; st.lin = n1; st.lout = L[1]; st.in_stride = L[2]; st.out_stride = L[2];
+        st.nb0 = L[2]; st.in_s0 = 1; st.out_s0 = 1;
+        st.nb1 = n0; st.in_s1 = (int64_t)n1 * L[2]; st.out_s1 = L12;
+        P->stage[1] = st;
+        P->stage_on[1] = true;
+        // S4: y inverse, B -> A
+        FftStage t = base(1, +1);
+        t.in = Bb; t.out = A; t.lin = L[1]; t.lout = n1; t.in_stride = L[2]; t.out_stride = L[2];
+        t.nb0 = L[2]; t.in_s0 = 1; t.out_s0 = 1;
+        t.nb1 = n0; t.in_s1 = L12; t.out_s1 = (int64_t)n1 * L[2];
+        P->stage[3] = t;
+        P->stage_on[3] = true;
+    }
+    {   // S3: x forward * khat * x inverse, in place on B
+        FftStage st = base(0, -1);
+        st.in = Bb; st.out = Bb; st.lin = n0; st.lout = n0; st.in_stride = L12; st.out_stride = L12;
+        st.nb0 = (int)L12; st.in_s0 = 1; st.out_s0 = 1;
+        st.nb1 = 1; st.in_s1 = 0; st.out_s1 = 0;
+        st.spec = P->khat; st.spec_stride = L12; st.spec_s0 = 1; st.spec_s1 = 0;
+        P->stage[2] = st;
+        P->stage_on[2] = true;
+    }
+    for (int k = 0; k < 5; ++k) {
+        FftStage& st = P->stage[k];
+        if (!P->stage_on[k]) continue;
+        st.B = std::max(1, std::min(st.nb0, 2048 / st.L));
+    }
+}
+
 void build(FftpimPlan* P) {
     const FftpimProblem& pr = P->prob;
     cudaStream_t s = P->build_stream;
@@ -370,9 +480,12 @@ void build(FftpimPlan* P) {
         fftpim_count_launch(1);
         launch_scale(P->khat, P->n_fft, 1.0 / (double)P->n_fft, s);   // numpy ifftn's 1/M
     }
-    P->work = dalloc<cplx>(P, P->n_fft);
-    P->pad_in = dalloc<cplx>(P, P->n_fft);
-    CK(cudaMemsetAsync(P->pad_in, 0, sizeof(cplx) * P->n_fft, s));   // padding stays zero: out-of-place forward FFT
+    setup_fft_pipeline(P, dims, s);
+    if (!P->custom_fft) {
+        P->work = dalloc<cplx>(P, P->n_fft);
+        P->pad_in = dalloc<cplx>(P, P->n_fft);
+        CK(cudaMemsetAsync(P->pad_in, 0, sizeof(cplx) * P->n_fft, s));   // padding stays zero: out-of-place forward FFT
+    }
     P->q_sorted = dalloc<cplx>(P, N);
 
     // ---- correction pairs (nearzone.py:245-256, 303-487)
@@ -721,6 +834,21 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.obs_start = P->obs_start;
     a.work = P->work;
     a.pad_in = P->pad_in;
+    if (P->custom_fft) {
+        a.k1_out = P->qg;
+        a.go1 = P->near_g.n[1];
+        a.go2 = P->near_g.n[2];
+        a.interp_grid = P->qg;
+        a.gi1 = a.go1;
+        a.gi2 = a.go2;
+    } else {
+        a.k1_out = P->pad_in;
+        a.go1 = P->cdims[1];
+        a.go2 = P->cdims[2];
+        a.interp_grid = P->work;
+        a.gi1 = a.go1;
+        a.gi2 = a.go2;
+    }
     a.khat = P->khat;
     a.n_fft = P->n_fft;
     a.pair_ptr = P->pair_ptr;
@@ -767,16 +895,31 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
         mark(3);
         if (parts & FFTPIM_NEAR) launch_near_project(a, s);
         mark(4);
-        if (parts & FFTPIM_NEAR) {
-            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
-            fftpim_count_launch(1);
-        }
-        mark(5);
-        if (parts & FFTPIM_NEAR) launch_spectrum_mul(a, s);
-        mark(6);
-        if (parts & FFTPIM_NEAR) {
-            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
-            fftpim_count_launch(1);
+        if (P->custom_fft) {
+            // stages 4/5/6 = forward z,y | fused x fwd*khat*inv | inverse y,z
+            if (parts & FFTPIM_NEAR) {
+                if (P->stage_on[0]) launch_fft_stage(P->stage[0], s);
+                if (P->stage_on[1]) launch_fft_stage(P->stage[1], s);
+            }
+            mark(5);
+            if (parts & FFTPIM_NEAR) launch_fft_stage(P->stage[2], s);
+            mark(6);
+            if (parts & FFTPIM_NEAR) {
+                if (P->stage_on[3]) launch_fft_stage(P->stage[3], s);
+                if (P->stage_on[4]) launch_fft_stage(P->stage[4], s);
+            }
+        } else {
+            if (parts & FFTPIM_NEAR) {
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+                fftpim_count_launch(1);
+            }
+            mark(5);
+            if (parts & FFTPIM_NEAR) launch_spectrum_mul(a, s);
+            mark(6);
+            if (parts & FFTPIM_NEAR) {
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+                fftpim_count_launch(1);
+            }
         }
         mark(7);
         if (parts & FFTPIM_NEAR) launch_corr_tiles(a, s);

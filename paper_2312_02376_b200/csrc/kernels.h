@@ -93,6 +93,10 @@ struct EvalArgs {
     const int* obs_start;
     cplx* work;
     cplx* pad_in;               // zero-padded FFT input; only the n^3 corner is written
+    cplx* k1_out;               // K1 target grid, indexed ((x*go1 + y)*go2 + z)
+    int go1, go2;
+    const cplx* interp_grid;    // near potentials on the grid, indexed ((x*gi1 + y)*gi2 + z)
+    int gi1, gi2;
     const cplx* khat;
     int64_t n_fft;
     const int64_t* pair_ptr;
@@ -124,6 +128,10 @@ void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);
 void launch_observers(const EvalArgs& a, cudaStream_t s);
+
+// ---- pruned column-FFT stages (fft_kernels.cu)
+size_t fft_stage_smem(const FftStage& st);
+void launch_fft_stage(const FftStage& st, cudaStream_t s);
 
 // ---- correction matvec (corr_kernels.cu)
 #define CORR_TILE 256

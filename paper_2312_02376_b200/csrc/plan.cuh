@@ -71,6 +71,25 @@ struct DevStatus {
     int pad_;
 };
 
+// One pruned column-FFT stage (fft_kernels.cu).
+struct FftStage {
+    const cplx* in;
+    cplx* out;
+    int L, lin, lout;           // transform length, nonzero inputs, kept outputs
+    int64_t in_stride, out_stride;   // along the transform axis
+    int nb0, nb1;               // columns: fast batch index (per block, B at a time) and grid.y
+    int64_t in_s0, out_s0, in_s1, out_s1;
+    int sign;                   // -1 forward, +1 inverse (ignored when spec is set)
+    const cplx* spec;           // fused x stage: forward, multiply by spec, inverse
+    int64_t spec_stride, spec_s0, spec_s1;
+    const cplx* tw;             // exp(-2 pi i t / L), t < L
+    const cplx* twp;            // per-pass compact twiddles, pass order
+    int ntwp;
+    int nrad;
+    int radix[24];
+    int B;                      // columns per block
+};
+
 struct FftpimPlan {
     FftpimProblem prob;           // copy (pointers cleared)
     FftpimInfo info;
@@ -117,6 +136,16 @@ struct FftpimPlan {
     unsigned char* pair_codeid = nullptr;  // (P) code id (export only)
     cplx* pair_coef = nullptr;    // (P) complex coefficients (dynamic / static-shifted)
     double* pair_coef_r = nullptr;  // (P) real coefficients (NPSP)
+    // pruned column-FFT pipeline (fft_kernels.cu); cuFFT full transforms otherwise
+    bool custom_fft = false;
+    cplx* qg = nullptr;           // (n0 n1 n2): K1 output, then the near potentials ug
+    cplx* fbufA = nullptr;        // (n0 n1 2n2)
+    cplx* fbufB = nullptr;        // (n0 2n1 2n2)
+    cplx* twiddle[3] = {nullptr, nullptr, nullptr};
+    cplx* twiddle_pass[3] = {nullptr, nullptr, nullptr};
+    int n_twiddle_pass[3] = {0, 0, 0};
+    bool stage_on[5] = {false, false, false, false, false};
+    FftStage stage[5];
     int64_t n_tiles = 0;          // CORR_TILE-pair tiles of the correction stream
     int64_t n_segments = 0;       // (observer, tile) segments
     unsigned* head_bits = nullptr;
