@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(128) k_pairs_fill(PairGeom pg, ImageSet im, Co
                     int64_t slot = out + __popc(mask & ((1u << lane) - 1u));
                     cplx v = pair_coefficient(pg, im, tabs, a, i, m, c, &bad);
                     a.pair_src[slot] = a.src_rank[c.orig];
-                    a.pair_codeid[slot] = (unsigned char)c.code;
+                    if (a.pair_codeid) a.pair_codeid[slot] = (unsigned char)c.code;
                     if (a.coef_r)
                         a.coef_r[slot] = v.re;
                     else

@@ -705,7 +705,8 @@ void build(FftpimPlan* P) {
     launch_code_tables(tb, pg.ncodes, pg, im, tables, tab_total, s);
     // fill pass
     P->pair_src = dalloc<int>(P, npairs);
-    P->pair_codeid = dalloc<unsigned char>(P, npairs);
+    // image codes are only needed for operand export; skipped for huge pair counts (C3/C4)
+    if (npairs <= (int64_t)1 << 31) P->pair_codeid = dalloc<unsigned char>(P, npairs);
     if (P->npsp)
         P->pair_coef_r = dalloc<double>(P, npairs);
     else
@@ -1082,6 +1083,7 @@ int fftpim_plan_export(const FftpimPlan* cplan, int32_t which, void* dst, int64_
         } else if (which == FFTPIM_PAIR_CODE) {
             need(npairs * 3);
             std::vector<unsigned char> cid(npairs);
+            if (!P->pair_codeid) throw Fail{FFTPIM_VALUE, "pair codes are not kept for plans with more than 2^31 pairs"};
             CK(cudaMemcpy(cid.data(), P->pair_codeid, npairs, cudaMemcpyDeviceToHost));
             signed char* o = (signed char*)dst;
             for (int64_t k = 0; k < npairs; ++k)

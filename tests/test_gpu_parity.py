@@ -157,3 +157,29 @@ def test_errors_map_to_reference_classes(fp):
     with pytest.raises(fp.WoodAnomalyError):
         fp.build_plan(cfg, fp.TargetBox((1, 1, 0.25)), fp.SourcePointSet(p2, np.ones(60)),
                       fp.ObserverPointSet(p2), fp.SolverParams(near_grid=(8, 8, 4)))
+
+
+@pytest.mark.parametrize("c", [5, 4, 3])
+def test_baseline_config_subset_parity(fp, c):
+    """C3/C4/C5 at full scale on the GPU against the reference run on a seeded
+    observer sample (tests/golden/make_subset_golden.py)."""
+    import os
+    from conftest import GOLDEN
+    from paper_2312_02376_b200.workloads import CONFIGS, c5_kshift, make_inputs
+    path = os.path.join(GOLDEN, f"c{c}_subset.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"no subset fixture for C{c}")
+    g = np.load(path)
+    w = CONFIGS[c]
+    pos, q = make_inputs(c)
+    kshift = w.kshift
+    if c == 5:
+        q, kshift = q[0], c5_kshift(0)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=kshift,
+                               regime=fp.Regime(w.regime))
+    plan = fp.build_plan(cfg, fp.TargetBox(w.D), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos),
+                         fp.SolverParams(**w.params()))
+    assert plan.far.kernel_terms == int(g["far_terms"])
+    assert rel_l2(plan.far.kernel, g["far_kernel"]) <= 1e-11
+    u = plan.evaluate(q)
+    assert rel_l2(u[g["obs_index"]], g["u"]) <= TOL
