@@ -77,7 +77,10 @@ __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
     a.k1_out[((int64_t)x * a.go1 + y) * a.go2 + z] = acc;
 }
 
+bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s);
+
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {
+    if (launch_near_project_tiled(a, s)) return;
     const int W = a.g.order + 1;
     const int b = nblk((int64_t)a.g.n[0] * a.g.n[1] * a.g.n[2], 256);
     switch (W) {
@@ -89,6 +92,149 @@ void launch_near_project(const EvalArgs& a, cudaStream_t s) {
         default: k_near_project<7><<<b, 256, 0, s>>>(a); break;
     }
     fftpim_count_launch();
+}
+
+// Tiled K1: a block owns a TX x TY x TZ tile of grid nodes (one thread each) and
+// first stages every point whose stencil can reach the tile -- the sorted points
+// of the start-cell columns (sx, sy) in the tile's reach, each a contiguous run
+// -- into shared memory (weights, z start, q) with coalesced loads.  The
+// per-node gather then reads shared memory only, in the same order as
+// k_near_project (ia, ib, ascending point), so both produce identical bits.
+// Tiles whose reach holds more than the staging capacity gather from global.
+#define K1_TX 4
+#define K1_TY 8
+#define K1_TZ 8
+template <int W>
+struct K1Tile {
+    static constexpr int RX = K1_TX + W - 1, RY = K1_TY + W - 1, RZ = K1_TZ + W - 1;
+    static constexpr int NCOL = RX * RY;
+    static constexpr int CAP = W <= 4 ? 512 : 768;
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) k_near_project_tiled(EvalArgs a) {
+    using T = K1Tile<W>;
+    extern __shared__ double k1s[];
+    double* sw = k1s;                                   // CAP x 3W weights
+    double* sq = sw + T::CAP * 3 * W;                   // CAP x 2 (q)
+    int* sz = reinterpret_cast<int*>(sq + T::CAP * 2);  // CAP z starts
+    int* cs = sz + T::CAP;                              // NCOL x (RZ + 1) local cell starts
+    int* coff = cs + T::NCOL * (T::RZ + 1);             // NCOL + 1 column offsets
+    int* cbase = coff + T::NCOL + 1;                    // NCOL global first index
+    const StencilGeom& g = a.g;
+    const int x0 = blockIdx.x * K1_TX, y0 = blockIdx.y * K1_TY, z0 = blockIdx.z * K1_TZ;
+    const int sx0 = x0 - (W - 1), sy0 = y0 - (W - 1), sz0 = z0 - (W - 1);
+    // column ranges (cells sz0 .. sz0 + RZ - 1, clipped)
+    const int zl = max(sz0, 0), zh = min(sz0 + T::RZ - 1, g.nc[2] - 1);
+    for (int c = threadIdx.x; c < T::NCOL; c += blockDim.x) {
+        const int sx = sx0 + c / T::RY, sy = sy0 + c % T::RY;
+        int lo = 0, hi = 0;
+        if (sx >= 0 && sx < g.nc[0] && sy >= 0 && sy < g.nc[1] && zl <= zh) {
+            const int k0 = (sx * g.nc[1] + sy) * g.nc[2];
+            lo = a.cell_start[k0 + zl];
+            hi = a.cell_start[k0 + zh + 1];
+            for (int j = 0; j <= T::RZ; ++j) {
+                const int zc = min(max(sz0 + j, zl), zh + 1);
+                cs[c * (T::RZ + 1) + j] = a.cell_start[k0 + zc] - lo;
+            }
+        } else {
+            for (int j = 0; j <= T::RZ; ++j) cs[c * (T::RZ + 1) + j] = 0;
+        }
+        cbase[c] = lo;
+        coff[c + 1] = hi - lo;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        coff[0] = 0;
+        for (int c = 0; c < T::NCOL; ++c) coff[c + 1] += coff[c];
+    }
+    __syncthreads();
+    const int total = coff[T::NCOL];
+    const bool staged = total <= T::CAP;
+    if (staged) {
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            int lo = 0, hi = T::NCOL;   // column of idx: coff[lo] <= idx < coff[lo+1]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (coff[mid] <= idx) lo = mid; else hi = mid;
+            }
+            const int64_t p = cbase[lo] + (idx - coff[lo]);
+            const double* w = a.src_w + p * 3 * W;
+#pragma unroll
+            for (int j = 0; j < 3 * W; ++j) sw[idx * 3 * W + j] = w[j];
+            const cplx qv = a.q_sorted[p];
+            sq[2 * idx] = qv.re;
+            sq[2 * idx + 1] = qv.im;
+            sz[idx] = a.src_start[3 * p + 2];
+        }
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x / (K1_TY * K1_TZ), y = y0 + (threadIdx.x / K1_TZ) % K1_TY, z = z0 + threadIdx.x % K1_TZ;
+    if (x >= g.n[0] || y >= g.n[1] || z >= g.n[2]) return;
+    cplx acc = mk(0.0);
+    const int zlo = max(z - (W - 1), 0), zhi = min(z, g.nc[2] - 1);
+    for (int ia = 0; ia < W; ++ia) {
+        const int sx = x - ia;
+        if (sx < 0 || sx >= g.nc[0] || zlo > zhi) continue;
+        for (int ib = 0; ib < W; ++ib) {
+            const int sy = y - ib;
+            if (sy < 0 || sy >= g.nc[1]) continue;
+            const int c = (sx - sx0) * T::RY + (sy - sy0);
+            if (staged) {
+                const int* cc = cs + c * (T::RZ + 1);
+                const int p0 = coff[c] + cc[zlo - sz0], p1 = coff[c] + cc[zhi + 1 - sz0];
+                for (int p = p0; p < p1; ++p) {
+                    const double* w = sw + p * 3 * W;
+                    const double wgt = (w[ia] * w[W + ib]) * w[2 * W + (z - sz[p])];
+                    acc.re += wgt * sq[2 * p];
+                    acc.im += wgt * sq[2 * p + 1];
+                }
+            } else {
+                const int k0 = (sx * g.nc[1] + sy) * g.nc[2];
+                const int p0 = a.cell_start[k0 + zlo], p1 = a.cell_start[k0 + zhi + 1];
+                for (int p = p0; p < p1; ++p) {
+                    const double* w = a.src_w + (int64_t)p * 3 * W;
+                    const int ic = z - a.src_start[3 * (int64_t)p + 2];
+                    const double wgt = (w[ia] * w[W + ib]) * w[2 * W + ic];
+                    const cplx qv = a.q_sorted[p];
+                    acc.re += wgt * qv.re;
+                    acc.im += wgt * qv.im;
+                }
+            }
+        }
+    }
+    a.k1_out[((int64_t)x * a.go1 + y) * a.go2 + z] = acc;
+}
+
+template <int W>
+static size_t k1_tiled_smem() {
+    using T = K1Tile<W>;
+    return (size_t)T::CAP * (3 * W + 2) * sizeof(double) + (size_t)T::CAP * sizeof(int) +
+           (size_t)(T::NCOL * (T::RZ + 1) + 2 * T::NCOL + 1) * sizeof(int);
+}
+
+template <int W>
+static void k1_tiled_launch(const EvalArgs& a, cudaStream_t s) {
+    const size_t smem = k1_tiled_smem<W>();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_near_project_tiled<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid((a.g.n[0] + K1_TX - 1) / K1_TX, (a.g.n[1] + K1_TY - 1) / K1_TY, (a.g.n[2] + K1_TZ - 1) / K1_TZ);
+    k_near_project_tiled<W><<<grid, K1_TX * K1_TY * K1_TZ, smem, s>>>(a);
+}
+
+bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s) {
+    if (a.g.n[0] < 2 || a.g.n[1] < 2 || a.g.n[2] < 2) return false;   // single-plane axes: global path
+    switch (a.g.order + 1) {
+        case 3: k1_tiled_launch<3>(a, s); break;
+        case 4: k1_tiled_launch<4>(a, s); break;
+        case 5: k1_tiled_launch<5>(a, s); break;
+        default: return false;
+    }
+    fftpim_count_launch();
+    return true;
 }
 
 // ---------------------------------------------------------------- K2

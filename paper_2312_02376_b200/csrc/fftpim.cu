@@ -797,7 +797,9 @@ void build(FftpimPlan* P) {
             throw Fail{FFTPIM_VALUE, "far grid too large for this build (max 3072 nodes, 32 along z)"};
         int warps = 8;
         while (warps > 1 && far_project_smem((int)nf, warps, pr.far_order) > 200 * 1024) --warps;
-        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, (N + 32 * warps - 1) / (32 * warps)));
+        // one wave of one block per SM: the per-block private grids are zeroed and
+        // reduced once per block, so fewer, longer-lived blocks are cheaper
+        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148, (N + 32 * warps - 1) / (32 * warps)));
         P->far_warps = warps;
         P->far_blocks = blocks;
         P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
@@ -877,10 +879,118 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     return a;
 }
 
+// Evaluation schedule.  For moderate pair counts the near-field chain (K1 + FFT
+// stages), the correction matvec K4 and the far chain run concurrently on three
+// plan-owned streams after the q permutation (K4 streams HBM while the FFT
+// stages are latency-bound) and join before the observer pass; for very large
+// pair streams (C3/C4) K4 needs the whole chip and the chains run in order.
+void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s) {
+    const bool concurrent = P->info.n_pairs <= 500000000LL;
+    if (!concurrent) {
+        if (parts & FFTPIM_NEAR && !P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
+        for (int64_t b = 0; b < batch; ++b) {
+            EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
+            launch_permute_q(a, s);
+            if (parts & FFTPIM_FAR) {
+                launch_far_project(a, s);
+                launch_far_sum(a, s);
+            }
+            if (parts & FFTPIM_NEAR) {
+                launch_near_project(a, s);
+                if (P->custom_fft) {
+                    for (int k = 0; k < 5; ++k)
+                        if (P->stage_on[k]) launch_fft_stage(P->stage[k], s);
+                } else {
+                    CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+                    launch_spectrum_mul(a, s);
+                    CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+                    fftpim_count_launch(2);
+                }
+                launch_corr_tiles(a, s);
+            }
+            launch_observers(a, s);
+        }
+        CK(cudaGetLastError());
+        return;
+    }
+    for (int64_t b = 0; b < batch; ++b) {
+        EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
+        launch_permute_q(a, s);
+        CK(cudaEventRecord(P->ev_fork, s));
+        cudaStream_t sn = P->aux[0], sc = P->aux[1], sf = P->aux[2];
+        if (parts & FFTPIM_NEAR) {
+            CK(cudaStreamWaitEvent(sn, P->ev_fork, 0));
+            launch_near_project(a, sn);
+            if (P->custom_fft) {
+                for (int k = 0; k < 5; ++k)
+                    if (P->stage_on[k]) launch_fft_stage(P->stage[k], sn);
+            } else {
+                CKFFT(cufftSetStream(P->fft_plan, sn));
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+                launch_spectrum_mul(a, sn);
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+                fftpim_count_launch(2);
+            }
+            CK(cudaEventRecord(P->ev_join[0], sn));
+            CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
+            launch_corr_tiles(a, sc);
+            CK(cudaEventRecord(P->ev_join[1], sc));
+            CK(cudaStreamWaitEvent(s, P->ev_join[0], 0));
+            CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));
+        }
+        if (parts & FFTPIM_FAR) {
+            CK(cudaStreamWaitEvent(sf, P->ev_fork, 0));
+            launch_far_project(a, sf);
+            launch_far_sum(a, sf);
+            CK(cudaEventRecord(P->ev_join[2], sf));
+            CK(cudaStreamWaitEvent(s, P->ev_join[2], 0));
+        }
+        launch_observers(a, s);
+    }
+    CK(cudaGetLastError());
+}
+
 void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s,
               cudaEvent_t* ev = nullptr) {
     if (parts & ~FFTPIM_ALL || parts == 0) throw Fail{FFTPIM_VALUE, "parts must be a non-empty subset of NEAR|FAR"};
     CK(cudaSetDevice(P->device));
+    if (!ev && s != nullptr && P->use_graphs) {
+        // replay a captured CUDA graph of the whole evaluation (launch-bound at small N);
+        // re-captured whenever the caller's buffers or the batch change
+        if (!(P->graph_exec && P->g_q == q && P->g_u == u && P->g_batch == batch && P->g_parts == parts)) {
+            if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);
+            P->graph_exec = nullptr;
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            P->capturing = true;
+            const long long l0 = g_launches.load();
+            try {
+                evaluate_schedule(P, q, u, batch, parts, s);
+                P->kernels_per_eval = (int)((g_launches.load() - l0) / batch);
+            } catch (...) {
+                P->capturing = false;
+                cudaStreamEndCapture(s, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            P->capturing = false;
+            CK(cudaStreamEndCapture(s, &graph));
+            CK(cudaGraphInstantiate(&P->graph_exec, graph, 0));
+            CK(cudaGraphDestroy(graph));
+            P->g_q = q;
+            P->g_u = u;
+            P->g_batch = batch;
+            P->g_parts = parts;
+        }
+        CK(cudaGraphLaunch(P->graph_exec, s));
+        fftpim_count_launch(P->kernels_per_eval * (int)batch);
+        CK(cudaGetLastError());
+        return;
+    }
+    if (!ev) {
+        evaluate_schedule(P, q, u, batch, parts, s);
+        return;
+    }
     if (parts & FFTPIM_NEAR) CKFFT(cufftSetStream(P->fft_plan, s));
     auto mark = [&](int k) {
         if (ev) CK(cudaEventRecord(ev[k], s));
@@ -950,9 +1060,13 @@ int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out) {
     try {
         P->prob = *p;
         P->device = p->device;
+        P->use_graphs = getenv("FFTPIM_NO_GRAPHS") == nullptr;
         memset(&P->info, 0, sizeof(P->info));
         CK(cudaSetDevice(P->device));
         CK(cudaStreamCreateWithFlags(&P->build_stream, cudaStreamNonBlocking));
+        for (auto& st : P->aux) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+        for (auto& e : P->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         P->status = dalloc<DevStatus>(P, 1);
         CK(cudaMemsetAsync(P->status, 0, sizeof(DevStatus), P->build_stream));
         build(P);
@@ -985,15 +1099,18 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
     try {
         CK(cudaSetDevice(plan->device));
         cudaStream_t s = plan->build_stream;
-        double *dq = nullptr, *du = nullptr;
+        // persistent staging buffers: stable pointers keep the captured graph valid
+        if (batch > plan->h_batch) {
+            dfree(plan, plan->h_q);
+            dfree(plan, plan->h_u);
+            plan->h_q = dalloc<double>(plan, 2 * plan->N * batch);
+            plan->h_u = dalloc<double>(plan, 2 * plan->M * batch);
+            plan->h_batch = batch;
+        }
         size_t qb = sizeof(double) * 2 * plan->N * batch, ub = sizeof(double) * 2 * plan->M * batch;
-        CK(cudaMallocAsync(&dq, qb, s));
-        CK(cudaMallocAsync(&du, ub, s));
-        CK(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, s));
-        evaluate(plan, dq, du, batch, parts, s);
-        CK(cudaMemcpyAsync(u, du, ub, cudaMemcpyDeviceToHost, s));
-        CK(cudaFreeAsync(dq, s));
-        CK(cudaFreeAsync(du, s));
+        CK(cudaMemcpyAsync(plan->h_q, q, qb, cudaMemcpyHostToDevice, s));
+        evaluate(plan, plan->h_q, plan->h_u, batch, parts, s);
+        CK(cudaMemcpyAsync(u, plan->h_u, ub, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         return FFTPIM_OK;
     } catch (const Fail& f) {
@@ -1130,7 +1247,16 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
     cudaSetDevice(plan->device);
     if (plan->build_stream) cudaStreamSynchronize(plan->build_stream);
     if (plan->fft_plan) cufftDestroy(plan->fft_plan);
+    if (plan->graph_exec) cudaGraphExecDestroy(plan->graph_exec);
     for (void* p : plan->allocations) cudaFree(p);
+    for (auto st : plan->aux)
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+    if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
+    for (auto e : plan->ev_join)
+        if (e) cudaEventDestroy(e);
     if (plan->build_stream) cudaStreamDestroy(plan->build_stream);
     delete plan;
 }

@@ -161,6 +161,25 @@ struct FftpimPlan {
     int far_blocks = 0;
     int far_warps = 0;
 
+    // CUDA graph of the evaluation schedule, keyed by the caller's buffers
+    bool use_graphs = true;
+    bool capturing = false;
+    cudaGraphExec_t graph_exec = nullptr;
+    const double* g_q = nullptr;
+    double* g_u = nullptr;
+    int64_t g_batch = 0;
+    int g_parts = 0;
+    int kernels_per_eval = 0;
+    // persistent device staging for fftpim_plan_evaluate_host
+    double* h_q = nullptr;
+    double* h_u = nullptr;
+    int64_t h_batch = 0;
+
+    // concurrent evaluation schedule (near chain | K4 | far chain)
+    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
+
     DevStatus* status = nullptr;
     int64_t device_bytes = 0;
     std::vector<void*> allocations;
