@@ -31,6 +31,16 @@ __device__ __forceinline__ cplx mul_si(cplx a, int sign) {
 // one Stockham pass of radix r over B columns of length L: y <- pass(x)
 __device__ __forceinline__ int ilog2_exact(int v) { return (v & (v - 1)) ? -1 : __ffs(v) - 1; }
 
+// XOR swizzle of a column index within its aligned 8-element (128 B) group:
+// stride-1, stride-4 and the 4-runs-at-16 patterns of the first Stockham passes
+// all land on distinct 16-byte bank slots.
+// (identity when L is not a multiple of 8: the last group would be partial)
+__device__ __forceinline__ int swz(int i, int L) {
+    if (L & 7) return i;
+    const int g = i >> 3;
+    return i ^ ((g ^ ((g >> 1) & 4)) & 7);
+}
+
 // q = v / d, returns v - q*d; shift/mask when d is a power of two (ld >= 0)
 __device__ __forceinline__ int divmod(int v, int d, int ld, int* q) {
     if (ld >= 0) {
@@ -66,42 +76,42 @@ __device__ void stockham_pass(const cplx* __restrict__ x, cplx* __restrict__ y, 
         cplx* yb = y + b * Lp;
         const int base = jp * p * r + k;
         if (r == 4) {
-            cplx a0 = xb[j], a1 = xb[j + m], a2 = xb[j + 2 * m], a3 = xb[j + 3 * m];
+            cplx a0 = xb[swz(j, L)], a1 = xb[swz(j + m, L)], a2 = xb[swz(j + 2 * m, L)], a3 = xb[swz(j + 3 * m, L)];
             if (k) {
                 a1 = a1 * twid(twp, k, sign);
                 a2 = a2 * twid(twp, p + k, sign);
                 a3 = a3 * twid(twp, 2 * p + k, sign);
             }
             const cplx t0 = a0 + a2, t1 = a0 - a2, t2 = a1 + a3, t3 = mul_si(a1 - a3, sign);
-            yb[base] = t0 + t2;
-            yb[base + p] = t1 + t3;
-            yb[base + 2 * p] = t0 - t2;
-            yb[base + 3 * p] = t1 - t3;
+            yb[swz(base, L)] = t0 + t2;
+            yb[swz(base + p, L)] = t1 + t3;
+            yb[swz(base + 2 * p, L)] = t0 - t2;
+            yb[swz(base + 3 * p, L)] = t1 - t3;
         } else if (r == 2) {
-            cplx a0 = xb[j], a1 = xb[j + m];
+            cplx a0 = xb[swz(j, L)], a1 = xb[swz(j + m, L)];
             if (k) a1 = a1 * twid(twp, k, sign);
-            yb[base] = a0 + a1;
-            yb[base + p] = a0 - a1;
+            yb[swz(base, L)] = a0 + a1;
+            yb[swz(base + p, L)] = a0 - a1;
         } else if (r == 3) {
-            cplx a0 = xb[j], a1 = xb[j + m], a2 = xb[j + 2 * m];
+            cplx a0 = xb[swz(j, L)], a1 = xb[swz(j + m, L)], a2 = xb[swz(j + 2 * m, L)];
             if (k) {
                 a1 = a1 * twid(twp, k, sign);
                 a2 = a2 * twid(twp, p + k, sign);
             }
             const cplx w1 = twid(tw, m, sign), w2 = twid(tw, 2 * m, sign);
-            yb[base] = a0 + a1 + a2;
-            yb[base + p] = a0 + w1 * a1 + w2 * a2;
-            yb[base + 2 * p] = a0 + w2 * a1 + w1 * a2;
+            yb[swz(base, L)] = a0 + a1 + a2;
+            yb[swz(base + p, L)] = a0 + w1 * a1 + w2 * a2;
+            yb[swz(base + 2 * p, L)] = a0 + w2 * a1 + w1 * a2;
         } else {
             cplx a[32];
             for (int q = 0; q < r; ++q) {
-                a[q] = xb[j + q * m];
+                a[q] = xb[swz(j + q * m, L)];
                 if (k && q) a[q] = a[q] * twid(twp, (q - 1) * p + k, sign);
             }
             for (int s = 0; s < r; ++s) {
                 cplx acc = a[0];
                 for (int q = 1; q < r; ++q) acc = acc + a[q] * twid(tw, (int)(((long long)q * s * m) % L), sign);
-                yb[base + s * p] = acc;
+                yb[swz(base + s * p, L)] = acc;
             }
         }
     }
@@ -142,13 +152,13 @@ __global__ void __launch_bounds__(256) k_fft_stage(FftStage st) {
         for (int idx = threadIdx.x; idx < B * L; idx += blockDim.x) {
             int b;
             const int i = divmod(idx, L, lL, &b);
-            x[b * Lp + i] = (b < nb && i < st.lin) ? st.in[in_base + b * st.in_s0 + i] : mk(0.0);
+            x[b * Lp + swz(i, L)] = (b < nb && i < st.lin) ? st.in[in_base + b * st.in_s0 + i] : mk(0.0);
         }
     } else {
         for (int idx = threadIdx.x; idx < B * L; idx += blockDim.x) {
             int i;
             const int b = divmod(idx, B, lB, &i);
-            x[b * Lp + i] = (b < nb && i < st.lin) ? st.in[in_base + b * st.in_s0 + (int64_t)i * st.in_stride] : mk(0.0);
+            x[b * Lp + swz(i, L)] = (b < nb && i < st.lin) ? st.in[in_base + b * st.in_s0 + (int64_t)i * st.in_stride] : mk(0.0);
         }
     }
     __syncthreads();
@@ -159,7 +169,7 @@ __global__ void __launch_bounds__(256) k_fft_stage(FftStage st) {
         for (int idx = threadIdx.x; idx < B * L; idx += blockDim.x) {
             int k;
             const int b = divmod(idx, B, lB, &k);
-            if (b < nb) r[b * Lp + k] = r[b * Lp + k] * st.spec[sp_base + b * st.spec_s0 + (int64_t)k * st.spec_stride];
+            if (b < nb) r[b * Lp + swz(k, L)] = r[b * Lp + swz(k, L)] * st.spec[sp_base + b * st.spec_s0 + (int64_t)k * st.spec_stride];
         }
         __syncthreads();
         cplx* o = (r == x) ? y : x;
@@ -171,13 +181,13 @@ __global__ void __launch_bounds__(256) k_fft_stage(FftStage st) {
         for (int idx = threadIdx.x; idx < B * st.lout; idx += blockDim.x) {
             int b;
             const int i = divmod(idx, st.lout, lo, &b);
-            if (b < nb) st.out[out_base + b * st.out_s0 + i] = r[b * Lp + i];
+            if (b < nb) st.out[out_base + b * st.out_s0 + i] = r[b * Lp + swz(i, L)];
         }
     } else {
         for (int idx = threadIdx.x; idx < B * st.lout; idx += blockDim.x) {
             int i;
             const int b = divmod(idx, B, lB, &i);
-            if (b < nb) st.out[out_base + b * st.out_s0 + (int64_t)i * st.out_stride] = r[b * Lp + i];
+            if (b < nb) st.out[out_base + b * st.out_s0 + (int64_t)i * st.out_stride] = r[b * Lp + swz(i, L)];
         }
     }
 }
