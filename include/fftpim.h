@@ -143,6 +143,26 @@ FFTPIM_API const char* fftpim_last_error(void);
 FFTPIM_API int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t parts,
                                    void* stream, double* stage_ms);
 
+/* ---- multi-GPU slab decomposition (no reference counterpart:
+ * the reference is single-process numpy).  The near grid is split into
+ * `world` x-slabs; shard r owns those planes, the observers (= sources) whose
+ * stencil starts there and their correction pairs, and 1/world of the FFT
+ * columns for the x transforms (NCCL all-to-all transposes; far-grid
+ * all-reduce; order-plane halo).  nccl_id != NULL: this process is shard `rank`
+ * on p->device, all processes pass the same 128-byte id from
+ * fftpim_nccl_unique_id.  nccl_id == NULL: all shards are emulated inside this
+ * process on p->device (exchanges become device copies).  Observers must be the
+ * sources; all three axes active. */
+typedef struct FftpimGroup FftpimGroup;
+FFTPIM_API int fftpim_nccl_unique_id(void* out, int64_t bytes);
+FFTPIM_API int fftpim_group_create(const FftpimProblem* p, int32_t world, int32_t rank, const void* nccl_id,
+                                   FftpimGroup** out);
+/* q: all n_src amplitudes (device); u: n_obs outputs (device) -- each process
+ * writes the observers its shard(s) own.  Stream ordered on `stream`. */
+FFTPIM_API int fftpim_group_evaluate(FftpimGroup* g, const double* q, double* u, void* stream);
+FFTPIM_API int fftpim_group_info(const FftpimGroup* g, int32_t shard, FftpimInfo* info);
+FFTPIM_API void fftpim_group_destroy(FftpimGroup* g);
+
 /* Number of kernel launches this library issued since load (evidence counter). */
 FFTPIM_API int64_t fftpim_launch_count(void);
 

@@ -48,7 +48,9 @@ class Info(C.Structure):
 
 EXPORTED = ("fftpim_plan_create", "fftpim_plan_evaluate", "fftpim_plan_evaluate_host",
             "fftpim_plan_info", "fftpim_plan_export", "fftpim_plan_set_far_kernel",
-            "fftpim_plan_destroy", "fftpim_last_error", "fftpim_launch_count", "fftpim_plan_profile")
+            "fftpim_plan_destroy", "fftpim_last_error", "fftpim_launch_count", "fftpim_plan_profile",
+            "fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
+            "fftpim_group_destroy")
 N_STAGES = 9
 STAGES = ("permute_q", "far_project", "far_sum", "near_project", "fft_forward", "spectrum_mul",
           "fft_inverse", "corr_matvec", "observers")
@@ -80,6 +82,14 @@ def load(path: str = LIB_PATH):
     lib.fftpim_plan_profile.argtypes = [vp, vp, vp, C.c_int32, vp, C.POINTER(C.c_double)]
     lib.fftpim_plan_destroy.argtypes = [vp]
     lib.fftpim_plan_destroy.restype = None
+    lib.fftpim_nccl_unique_id.argtypes = [vp, C.c_int64]
+    lib.fftpim_group_create.argtypes = [C.POINTER(Problem), C.c_int32, C.c_int32, vp, C.POINTER(vp)]
+    lib.fftpim_group_evaluate.argtypes = [vp, vp, vp, vp]
+    lib.fftpim_group_info.argtypes = [vp, C.c_int32, C.POINTER(Info)]
+    lib.fftpim_group_destroy.argtypes = [vp]
+    lib.fftpim_group_destroy.restype = None
+    for name in ("fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info"):
+        getattr(lib, name).restype = C.c_int
     lib.fftpim_last_error.restype = C.c_char_p
     lib.fftpim_launch_count.restype = C.c_int64
     for name in ("fftpim_plan_create", "fftpim_plan_evaluate", "fftpim_plan_evaluate_host",

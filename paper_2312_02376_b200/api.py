@@ -50,6 +50,38 @@ def _same_points(src: SourcePointSet, obs: ObserverPointSet) -> bool:
         src.positions.shape == obs.positions.shape and np.array_equal(src.positions, obs.positions))
 
 
+def problem_struct(cfg: PeriodicityConfig, box: TargetBox, src: SourcePointSet, obs: ObserverPointSet,
+                   params: SolverParams, device: int | None = None):
+    """FftpimProblem for the C ABI; returns (struct, same_points, arrays to keep alive)."""
+    same = _same_points(src, obs)
+    pr = nat.Problem()
+    pr.dim = cfg.dim.value
+    pr.regime = REGIME_CODE[cfg.regime]
+    for a in range(3):
+        pr.L[a] = cfg.L[a]
+        pr.D[a] = box.D[a]
+        pr.kshift[a][0] = cfg.kshift[a].real
+        pr.kshift[a][1] = cfg.kshift[a].imag
+        pr.far_grid[a] = params.far_grid[a]
+    pr.k0[0], pr.k0[1] = cfg.k0.real, cfg.k0.imag
+    pr.i_d = params.i_d
+    pr.near_order = params.near_order
+    dims = params.resolve_near_grid(max(len(src), len(obs)), box)
+    for a in range(3):
+        pr.near_grid[a] = int(dims[a])
+    pr.far_order = params.far_order
+    pr.series_tol = params.series_tol
+    pr.er_range_boxes = params.er_range_boxes
+    sp = np.ascontiguousarray(src.positions, dtype=np.float64)
+    op = sp if same else np.ascontiguousarray(obs.positions, dtype=np.float64)
+    pr.n_src, pr.n_obs = len(src), len(obs)
+    pr.src_pos = sp.ctypes.data
+    pr.obs_pos = None if same else op.ctypes.data
+    pr.same_points = int(same)
+    pr.device = _default_device() if device is None else int(device)
+    return pr, same, (sp, op)
+
+
 class NativePlan:
     """Owns one libfftpim plan (device memory lives until this object dies)."""
 

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
         for (int c = 0; c < W; ++c) wz[c] = w[2 * W + c];
         for (int ia = sub; ia < W; ia += OBS_LPO) {
             const double wx = w[ia];
-            const int64_t xo = (int64_t)min(s0 + ia, m0) * c1;
+            const int64_t xo = (int64_t)(min(s0 + ia, m0) - a.gx0) * c1;
 #pragma unroll
             for (int ib = 0; ib < W; ++ib) {
                 const double wxy = wx * w[W + ib];

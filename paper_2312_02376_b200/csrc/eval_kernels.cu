@@ -42,8 +42,9 @@ template <int W>
 __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const StencilGeom& g = a.g;
-    if (t >= (int64_t)g.n[0] * g.n[1] * g.n[2]) return;
-    const int z = (int)(t % g.n[2]), y = (int)((t / g.n[2]) % g.n[1]), x = (int)(t / ((int64_t)g.n[1] * g.n[2]));
+    if (t >= (int64_t)a.knx * g.n[1] * g.n[2]) return;
+    const int z = (int)(t % g.n[2]), y = (int)((t / g.n[2]) % g.n[1]),
+              x = (int)(t / ((int64_t)g.n[1] * g.n[2])) + a.kx0;
     cplx acc = mk(0.0);
     {
         const int wx = g.w[0], wy = g.w[1], wz = g.w[2];
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
             }
         }
     }
-    a.k1_out[((int64_t)x * a.go1 + y) * a.go2 + z] = acc;
+    a.k1_out[((int64_t)(x - a.kx0) * a.go1 + y) * a.go2 + z] = acc;
 }
 
 bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s);
@@ -82,7 +83,7 @@ bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s);
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {
     if (launch_near_project_tiled(a, s)) return;
     const int W = a.g.order + 1;
-    const int b = nblk((int64_t)a.g.n[0] * a.g.n[1] * a.g.n[2], 256);
+    const int b = nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], 256);
     switch (W) {
         case 2: k_near_project<2><<<b, 256, 0, s>>>(a); break;
         case 3: k_near_project<3><<<b, 256, 0, s>>>(a); break;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) k_near_project_tiled(EvalArgs a) {
     int* coff = cs + T::NCOL * (T::RZ + 1);             // NCOL + 1 column offsets
     int* cbase = coff + T::NCOL + 1;                    // NCOL global first index
     const StencilGeom& g = a.g;
-    const int x0 = blockIdx.x * K1_TX, y0 = blockIdx.y * K1_TY, z0 = blockIdx.z * K1_TZ;
+    const int x0 = a.kx0 + blockIdx.x * K1_TX, y0 = blockIdx.y * K1_TY, z0 = blockIdx.z * K1_TZ;
     const int sx0 = x0 - (W - 1), sy0 = y0 - (W - 1), sz0 = z0 - (W - 1);
     // column ranges (cells sz0 .. sz0 + RZ - 1, clipped)
     const int zl = max(sz0, 0), zh = min(sz0 + T::RZ - 1, g.nc[2] - 1);
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256) k_near_project_tiled(EvalArgs a) {
     }
     __syncthreads();
     const int x = x0 + threadIdx.x / (K1_TY * K1_TZ), y = y0 + (threadIdx.x / K1_TZ) % K1_TY, z = z0 + threadIdx.x % K1_TZ;
-    if (x >= g.n[0] || y >= g.n[1] || z >= g.n[2]) return;
+    if (x >= a.kx0 + a.knx || y >= g.n[1] || z >= g.n[2]) return;
     cplx acc = mk(0.0);
     const int zlo = max(z - (W - 1), 0), zhi = min(z, g.nc[2] - 1);
     for (int ia = 0; ia < W; ++ia) {
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(256) k_near_project_tiled(EvalArgs a) {
             }
         }
     }
-    a.k1_out[((int64_t)x * a.go1 + y) * a.go2 + z] = acc;
+    a.k1_out[((int64_t)(x - a.kx0) * a.go1 + y) * a.go2 + z] = acc;
 }
 
 template <int W>
@@ -221,7 +222,7 @@ static void k1_tiled_launch(const EvalArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(k_near_project_tiled<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    dim3 grid((a.g.n[0] + K1_TX - 1) / K1_TX, (a.g.n[1] + K1_TY - 1) / K1_TY, (a.g.n[2] + K1_TZ - 1) / K1_TZ);
+    dim3 grid((a.knx + K1_TX - 1) / K1_TX, (a.g.n[1] + K1_TY - 1) / K1_TY, (a.g.n[2] + K1_TZ - 1) / K1_TZ);
     k_near_project_tiled<W><<<grid, K1_TX * K1_TY * K1_TZ, smem, s>>>(a);
 }
 
@@ -235,6 +236,16 @@ bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s) {
     }
     fftpim_count_launch();
     return true;
+}
+
+__global__ void k_axpy(cplx* __restrict__ acc, const cplx* __restrict__ x, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) acc[i] = acc[i] + x[i];
+}
+void launch_axpy(cplx* acc, const cplx* x, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    k_axpy<<<nblk(n, 256), 256, 0, s>>>(acc, x, n);
+    fftpim_count_launch();
 }
 
 // ---------------------------------------------------------------- K2
@@ -269,13 +280,13 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
     cplx* mine = sgrid + warp * nf;
     const int wfx = a.fs.w[0], wfy = a.fs.w[1], wfz = a.fs.w[2];
     const int64_t stride = (int64_t)gridDim.x * warps * 32;
-    for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < a.N; base += stride) {
+    for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < a.far_n; base += stride) {
         const int64_t p = base + lane;
-        if (p < a.N) {
+        if (p < a.far_n) {
             const double* w = a.src_fw + p * 3 * WF;
 #pragma unroll
             for (int j = 0; j < 3 * WF; ++j) stage[lane * REC + j] = w[j];
-            const cplx qv = a.q_sorted[p];
+            const cplx qv = a.far_q[p];
             stage[lane * REC + 3 * WF] = qv.re;
             stage[lane * REC + 3 * WF + 1] = qv.im;
             sstart[lane * 3] = a.src_fstart[3 * p];
@@ -283,7 +294,7 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
             sstart[lane * 3 + 2] = a.src_fstart[3 * p + 2];
         }
         __syncwarp();
-        const int cnt = (int)min((int64_t)32, a.N - base);
+        const int cnt = (int)min((int64_t)32, a.far_n - base);
         for (int j = 0; j < cnt; ++j) {
             const double* r = stage + j * REC;
             const int s0 = sstart[3 * j], s1 = sstart[3 * j + 1], s2 = sstart[3 * j + 2];

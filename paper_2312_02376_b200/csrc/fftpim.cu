@@ -5,6 +5,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -320,6 +321,55 @@ void setup_fft_pipeline(FftpimPlan* P, const int dims[3], cudaStream_t s) {
     }
 }
 
+// Slab-shard version of the pruned pipeline: z and y transforms on the shard's
+// own x-planes, then an all-to-all transpose to FFT columns [C0, C1) for the
+// fused x stage (its khat slice only), the transpose back, y/z inverses, and a
+// halo of order planes from the next shard for the interpolation.
+void setup_fft_pipeline_shard(FftpimPlan* P, const int dims[3], cudaStream_t s) {
+    if (!P->custom_fft) throw Fail{FFTPIM_VALUE, "slab-decomposed plans need FFT lengths with prime factors <= 31"};
+    if (dims[1] < 2 || dims[2] < 2) throw Fail{FFTPIM_VALUE, "slab-decomposed plans need three active axes"};
+    const int G = P->world, n0 = dims[0], n1 = dims[1], n2 = dims[2];
+    const int L0 = P->cdims[0], L1 = P->cdims[1], L2 = P->cdims[2];
+    const int nl = P->n0_loc;
+    P->C = (int64_t)L1 * L2;
+    P->col_start.resize(G + 1);
+    for (int r = 0; r <= G; ++r) P->col_start[r] = (int64_t)r * P->C / G;
+    P->C0 = P->col_start[P->rank];
+    P->C1 = P->col_start[P->rank + 1];
+    const int64_t ncol = P->C1 - P->C0;
+    // replace the full-domain buffers by slab buffers
+    dfree(P, P->qg);
+    dfree(P, P->fbufA);
+    dfree(P, P->fbufB);
+    P->qg = dalloc<cplx>(P, (int64_t)(nl + P->halo) * n1 * n2);
+    P->fbufA = dalloc<cplx>(P, (int64_t)nl * n1 * L2);
+    P->fbufB = dalloc<cplx>(P, (int64_t)nl * L1 * L2);
+    P->a2a_send = dalloc<cplx>(P, (int64_t)nl * P->C);
+    P->a2a_recv = dalloc<cplx>(P, (int64_t)n0 * ncol);
+    // khat slice [kx][own columns]
+    cplx* ks = dalloc<cplx>(P, (int64_t)L0 * ncol);
+    CK(cudaMemcpy2DAsync(ks, ncol * sizeof(cplx), P->khat + P->C0, P->C * sizeof(cplx), ncol * sizeof(cplx), L0,
+                         cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(P, P->khat);
+    P->khat = ks;
+    FftStage* st = P->stage;
+    // S1: z forward, qg (own planes) -> A
+    st[0].in = P->qg; st[0].out = P->fbufA; st[0].nb1 = nl;
+    // S2: y forward, A -> B
+    st[1].in = P->fbufA; st[1].out = P->fbufB; st[1].nb1 = nl;
+    // S3: x fused on the transposed columns: recv[x][c_local]
+    st[2].in = P->a2a_recv; st[2].out = P->a2a_recv; st[2].lin = n0; st[2].lout = n0;
+    st[2].in_stride = ncol; st[2].out_stride = ncol; st[2].nb0 = (int)ncol; st[2].in_s0 = 1; st[2].out_s0 = 1;
+    st[2].spec = P->khat; st[2].spec_stride = ncol; st[2].spec_s0 = 1;
+    st[2].B = std::max(1, std::min(st[2].nb0, 2048 / st[2].L));
+    // S4: y inverse, B -> A
+    st[3].in = P->fbufB; st[3].out = P->fbufA; st[3].nb1 = nl;
+    // S5: z inverse, A -> qg (own planes, the halo planes follow)
+    st[4].in = P->fbufA; st[4].out = P->qg; st[4].nb1 = nl;
+    (void)L0;
+}
+
 void build(FftpimPlan* P) {
     const FftpimProblem& pr = P->prob;
     cudaStream_t s = P->build_stream;
@@ -463,6 +513,38 @@ void build(FftpimPlan* P) {
     launch_stencils(d_obs, P->obs_perm, M, P->far_og, P->obs_fw, P->obs_fstart, P->status, 23, s);
     check_status(P, "stencil construction");
 
+    // ---- slab ownership: planes [X0, X1), observers/sources whose
+    // near stencil starts there = one contiguous range of the x-major sorted order
+    P->i0 = 0;
+    P->i1 = M;
+    P->X0 = 0;
+    P->X1 = dims[0];
+    P->n0_loc = dims[0];
+    P->halo = 0;
+    if (P->sharded) {
+        if (!same) throw Fail{FFTPIM_VALUE, "slab-decomposed plans need observers == sources"};
+        const int G = P->world;
+        P->plane_start.resize(G + 1);
+        for (int r = 0; r <= G; ++r) P->plane_start[r] = (int)((int64_t)r * dims[0] / G);
+        P->X0 = P->plane_start[P->rank];
+        P->X1 = P->plane_start[P->rank + 1];
+        P->n0_loc = P->X1 - P->X0;
+        for (int r = 0; r + 1 < G; ++r)
+            if (P->plane_start[r + 1] - P->plane_start[r] < W - 1)
+                throw Fail{FFTPIM_VALUE, "too many slab shards for the near grid (need >= order planes each)"};
+        P->halo = P->rank + 1 < G ? W - 1 : 0;
+        auto first_sorted = [&](int sx) -> int64_t {
+            if (sx >= P->near_g.nc[0]) return N;
+            int v = 0;
+            CK(cudaMemcpy(&v, P->cell_start + (int64_t)sx * P->near_g.nc[1] * P->near_g.nc[2], sizeof(int),
+                          cudaMemcpyDeviceToHost));
+            return v;
+        };
+        P->i0 = first_sorted(P->X0);
+        P->i1 = first_sorted(P->X1);
+    }
+    const int64_t Mown = P->i1 - P->i0;
+
     // ---- near kernel table -> kernel_hat (nearzone.py:215-235)
     P->khat = dalloc<cplx>(P, P->n_fft);
     launch_embed_table(P->khat, P->cdims, dims, h, im, s);
@@ -481,6 +563,7 @@ void build(FftpimPlan* P) {
         launch_scale(P->khat, P->n_fft, 1.0 / (double)P->n_fft, s);   // numpy ifftn's 1/M
     }
     setup_fft_pipeline(P, dims, s);
+    if (P->sharded) setup_fft_pipeline_shard(P, dims, s);
     if (!P->custom_fft) {
         P->work = dalloc<cplx>(P, P->n_fft);
         P->pad_in = dalloc<cplx>(P, P->n_fft);
@@ -630,21 +713,21 @@ void build(FftpimPlan* P) {
     PairArgs pa{};
     pa.src_pos = d_src;
     pa.obs_pos = d_obs;
-    pa.obs_perm = P->obs_perm;
-    pa.M = M;
+    pa.obs_perm = P->obs_perm + P->i0;
+    pa.M = Mown;
     pa.box_start = box_start;
     pa.box_order = box_order;
     pa.aug_orig = aug_orig;
     pa.aug_code = aug_code;
-    pa.obs_start = P->obs_start;
-    pa.obs_w = P->obs_w;
+    pa.obs_start = P->obs_start + 3 * P->i0;
+    pa.obs_w = P->obs_w + P->i0 * 3 * W;
     pa.src_start = P->src_start;
     pa.src_w = P->src_w;
     pa.src_rank = P->src_rank;
     pa.W = W;
     for (int a = 0; a < 3; ++a) pa.wdt[a] = P->near_g.w[a];
     pa.st = P->status;
-    int64_t* counts = dalloc<int64_t>(P, M + 1);
+    int64_t* counts = dalloc<int64_t>(P, Mown + 1);
     int* d0mm = dalloc<int>(P, 2 * 81);
     {
         std::vector<int> init(162);
@@ -661,21 +744,21 @@ void build(FftpimPlan* P) {
     pa.tallies = d_cnt + 1;
     launch_pairs_count(pg, pa, s);
     check_status(P, "correction pair discovery");
-    P->pair_ptr = dalloc<int64_t>(P, M + 1);
+    P->pair_ptr = dalloc<int64_t>(P, Mown + 1);
     {
         size_t bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, P->pair_ptr, (int)(M + 1), s);
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, P->pair_ptr, (int)(Mown + 1), s);
         void* tmp = nullptr;
         CK(cudaMallocAsync(&tmp, bytes + 16, s));
-        CK(cudaMemsetAsync(counts + M, 0, sizeof(int64_t), s));
-        cub::DeviceScan::ExclusiveSum(tmp, bytes, counts, P->pair_ptr, (int)(M + 1), s);
+        CK(cudaMemsetAsync(counts + Mown, 0, sizeof(int64_t), s));
+        cub::DeviceScan::ExclusiveSum(tmp, bytes, counts, P->pair_ptr, (int)(Mown + 1), s);
         fftpim_count_launch(2);
         CK(cudaFreeAsync(tmp, s));
     }
     int64_t npairs = 0;
     unsigned long long tallies[3];
     std::vector<int> mm(162);
-    CK(cudaMemcpyAsync(&npairs, P->pair_ptr + M, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&npairs, P->pair_ptr + Mown, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(tallies, d_cnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(mm.data(), d0mm, sizeof(int) * 162, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -721,11 +804,11 @@ void build(FftpimPlan* P) {
     launch_pairs_fill(pg, im, tb, pa, s);
     P->n_tiles = (npairs + CORR_TILE - 1) / CORR_TILE;
     P->head_bits = dalloc<unsigned>(P, (npairs + 31) / 32 + 8);
-    P->seg_first = dalloc<int64_t>(P, M + 1);
+    P->seg_first = dalloc<int64_t>(P, Mown + 1);
     P->seg_base = dalloc<int64_t>(P, P->n_tiles);
     {
-        int64_t* spans = dalloc<int64_t>(P, M + 1);
-        build_corr_metadata(P->pair_ptr, M, npairs, P->n_tiles, P->head_bits, P->seg_first, P->seg_base, spans,
+        int64_t* spans = dalloc<int64_t>(P, Mown + 1);
+        build_corr_metadata(P->pair_ptr, Mown, npairs, P->n_tiles, P->head_bits, P->seg_first, P->seg_base, spans,
                             &P->n_segments, s);
         dfree(P, spans);
     }
@@ -799,7 +882,7 @@ void build(FftpimPlan* P) {
         while (warps > 1 && far_project_smem((int)nf, warps, pr.far_order) > 200 * 1024) --warps;
         // one wave of one block per SM: the per-block private grids are zeroed and
         // reduced once per block, so fewer, longer-lived blocks are cheaper
-        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148, (N + 32 * warps - 1) / (32 * warps)));
+        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148, (Mown + 32 * warps - 1) / (32 * warps)));
         P->far_warps = warps;
         P->far_blocks = blocks;
         P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
@@ -875,7 +958,31 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.far_ug = P->far_ug;
     a.far_blocks = P->far_blocks;
     a.far_warps = P->far_warps;
+    a.far_q = P->q_sorted;
+    a.far_n = P->N;
+    a.kx0 = 0;
+    a.knx = P->near_g.n[0];
+    a.gx0 = 0;
     a.parts = parts;
+    if (P->sharded) {
+        // slab shard: own planes for K1/interp, own observers (= own sources) for
+        // K4, interpolation and the far projection partial
+        const int64_t i0 = P->i0;
+        const int W = P->near_g.order + 1, WF = P->far_sg.order + 1;
+        a.M = P->i1 - P->i0;
+        a.obs_perm = P->obs_perm + i0;
+        a.obs_w = P->obs_w + i0 * 3 * W;
+        a.obs_start = P->obs_start + 3 * i0;
+        a.obs_fw = P->obs_fw + i0 * 3 * WF;
+        a.obs_fstart = P->obs_fstart + 3 * i0;
+        a.src_fw = P->src_fw + i0 * 3 * WF;
+        a.src_fstart = P->src_fstart + 3 * i0;
+        a.far_q = P->q_sorted + i0;
+        a.far_n = P->i1 - P->i0;
+        a.kx0 = P->X0;
+        a.knx = P->n0_loc;
+        a.gx0 = P->X0;
+    }
     return a;
 }
 
@@ -1041,6 +1148,155 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
     CK(cudaGetLastError());
 }
 
+// ------------------------------------------------------------------ slab groups
+// A group is the slab decomposition of one problem over `world` shards: either
+// one shard per process/GPU with NCCL over NVLink (the all-to-all transposes,
+// the 16 KB far-grid all-reduce, the halo), or all shards emulated inside one
+// process on one device (exchanges become device copies) -- the single-GPU
+// check of the decomposition math.
+#define NCK(x)                                                                                     \
+    do {                                                                                           \
+        ncclResult_t r_ = (x);                                                                     \
+        if (r_ != ncclSuccess) throw Fail{FFTPIM_CUDA, std::string(#x) + ": " + ncclGetErrorString(r_)}; \
+    } while (0)
+
+struct GroupImpl {
+    int world = 1, rank = 0;
+    bool emulate = true;
+    std::vector<FftpimPlan*> shards;   // emulate: all shards; NCCL: this rank's shard
+    ncclComm_t comm = nullptr;
+};
+
+void shard_phase1(FftpimPlan* P, const EvalArgs& a, cudaStream_t s) {
+    launch_permute_q(a, s);
+    launch_near_project(a, s);
+    launch_fft_stage(P->stage[0], s);
+    launch_fft_stage(P->stage[1], s);
+    // pack the own planes' columns per destination shard: send[r][xl][c - C_r]
+    const int nl = P->n0_loc;
+    int64_t off = 0;
+    for (int r = 0; r < P->world; ++r) {
+        const int64_t nc = P->col_start[r + 1] - P->col_start[r];
+        CK(cudaMemcpy2DAsync(P->a2a_send + off, nc * sizeof(cplx), P->fbufB + P->col_start[r], P->C * sizeof(cplx),
+                             nc * sizeof(cplx), nl, cudaMemcpyDeviceToDevice, s));
+        off += (int64_t)nl * nc;
+    }
+    launch_far_project(a, s);
+}
+
+void shard_phase3(FftpimPlan* P, const EvalArgs& a, cudaStream_t s) {
+    // unpack send[r][xl][c - C_r] -> B[xl][c]
+    const int nl = P->n0_loc;
+    int64_t off = 0;
+    for (int r = 0; r < P->world; ++r) {
+        const int64_t nc = P->col_start[r + 1] - P->col_start[r];
+        CK(cudaMemcpy2DAsync(P->fbufB + P->col_start[r], P->C * sizeof(cplx), P->a2a_send + off, nc * sizeof(cplx),
+                             nc * sizeof(cplx), nl, cudaMemcpyDeviceToDevice, s));
+        off += (int64_t)nl * nc;
+    }
+    launch_fft_stage(P->stage[3], s);
+    launch_fft_stage(P->stage[4], s);
+    launch_far_sum(a, s);
+}
+
+void group_evaluate(GroupImpl* G, const double* q, double* u, cudaStream_t s) {
+    const int W = G->world;
+    std::vector<EvalArgs> args;
+    for (auto* P : G->shards) {
+        CK(cudaSetDevice(P->device));
+        args.push_back(eval_args(P, q, u, FFTPIM_ALL));
+    }
+    const int ns = (int)G->shards.size();
+    for (int k = 0; k < ns; ++k) shard_phase1(G->shards[k], args[k], s);
+    // forward transpose + far-grid all-reduce
+    if (G->emulate) {
+        for (int r = 0; r < W; ++r) {
+            FftpimPlan* src = G->shards[r];
+            int64_t off = 0;
+            for (int d = 0; d < W; ++d) {
+                FftpimPlan* dst = G->shards[d];
+                const int64_t nc = src->col_start[d + 1] - src->col_start[d];
+                const int64_t cnt = (int64_t)src->n0_loc * nc;
+                CK(cudaMemcpyAsync(dst->a2a_recv + (int64_t)src->X0 * nc, src->a2a_send + off, cnt * sizeof(cplx),
+                                   cudaMemcpyDeviceToDevice, s));
+                off += cnt;
+            }
+        }
+        FftpimPlan* P0 = G->shards[0];
+        const int64_t nf = P0->n_far;
+        for (int r = 1; r < W; ++r) launch_axpy(P0->far_qg, G->shards[r]->far_qg, nf, s);
+        for (int r = 1; r < W; ++r)
+            CK(cudaMemcpyAsync(G->shards[r]->far_qg, P0->far_qg, nf * sizeof(cplx), cudaMemcpyDeviceToDevice, s));
+    } else {
+        FftpimPlan* P = G->shards[0];
+        const int64_t ncol = P->C1 - P->C0;
+        NCK(ncclGroupStart());
+        int64_t off = 0;
+        for (int d = 0; d < W; ++d) {
+            const int64_t nc = P->col_start[d + 1] - P->col_start[d];
+            const int64_t cnt = (int64_t)P->n0_loc * nc;
+            NCK(ncclSend(P->a2a_send + off, 2 * cnt, ncclDouble, d, G->comm, s));
+            const int64_t rcnt = (int64_t)(P->plane_start[d + 1] - P->plane_start[d]) * ncol;
+            NCK(ncclRecv(P->a2a_recv + (int64_t)P->plane_start[d] * ncol, 2 * rcnt, ncclDouble, d, G->comm, s));
+            off += cnt;
+        }
+        NCK(ncclGroupEnd());
+        NCK(ncclAllReduce(P->far_qg, P->far_qg, 2 * P->n_far, ncclDouble, ncclSum, G->comm, s));
+    }
+    for (int k = 0; k < ns; ++k) launch_fft_stage(G->shards[k]->stage[2], s);
+    // backward transpose: recv rows of shard r's planes -> r's send[d-block]
+    if (G->emulate) {
+        for (int d = 0; d < W; ++d) {
+            FftpimPlan* src = G->shards[d];
+            const int64_t nc = src->C1 - src->C0;
+            for (int r = 0; r < W; ++r) {
+                FftpimPlan* dst = G->shards[r];
+                int64_t off = 0;
+                for (int k = 0; k < d; ++k) off += (int64_t)dst->n0_loc * (dst->col_start[k + 1] - dst->col_start[k]);
+                CK(cudaMemcpyAsync(dst->a2a_send + off, src->a2a_recv + (int64_t)dst->X0 * nc,
+                                   (int64_t)dst->n0_loc * nc * sizeof(cplx), cudaMemcpyDeviceToDevice, s));
+            }
+        }
+    } else {
+        FftpimPlan* P = G->shards[0];
+        const int64_t ncol = P->C1 - P->C0;
+        NCK(ncclGroupStart());
+        int64_t off = 0;
+        for (int d = 0; d < W; ++d) {
+            const int64_t nc = P->col_start[d + 1] - P->col_start[d];
+            const int64_t scnt = (int64_t)(P->plane_start[d + 1] - P->plane_start[d]) * ncol;
+            NCK(ncclSend(P->a2a_recv + (int64_t)P->plane_start[d] * ncol, 2 * scnt, ncclDouble, d, G->comm, s));
+            NCK(ncclRecv(P->a2a_send + off, 2 * (int64_t)P->n0_loc * nc, ncclDouble, d, G->comm, s));
+            off += (int64_t)P->n0_loc * nc;
+        }
+        NCK(ncclGroupEnd());
+    }
+    for (int k = 0; k < ns; ++k) shard_phase3(G->shards[k], args[k], s);
+    // halo: the first `order` planes of shard r+1 follow shard r's own planes
+    if (G->emulate) {
+        for (int r = 0; r + 1 < W; ++r) {
+            FftpimPlan* dst = G->shards[r];
+            FftpimPlan* src = G->shards[r + 1];
+            const int64_t plane = (int64_t)dst->near_g.n[1] * dst->near_g.n[2];
+            CK(cudaMemcpyAsync(dst->qg + (int64_t)dst->n0_loc * plane, src->qg, dst->halo * plane * sizeof(cplx),
+                               cudaMemcpyDeviceToDevice, s));
+        }
+    } else {
+        FftpimPlan* P = G->shards[0];
+        const int64_t plane = (int64_t)P->near_g.n[1] * P->near_g.n[2];
+        const int Wh = P->near_g.order;   // halo planes = order
+        NCK(ncclGroupStart());
+        if (G->rank > 0) NCK(ncclSend(P->qg, 2 * Wh * plane, ncclDouble, G->rank - 1, G->comm, s));
+        if (G->rank + 1 < W) NCK(ncclRecv(P->qg + (int64_t)P->n0_loc * plane, 2 * Wh * plane, ncclDouble, G->rank + 1, G->comm, s));
+        NCK(ncclGroupEnd());
+    }
+    for (int k = 0; k < ns; ++k) {
+        launch_corr_tiles(args[k], s);
+        launch_observers(args[k], s);
+    }
+    CK(cudaGetLastError());
+}
+
 int fail(const Fail& f) {
     g_last_error = f.msg;
     return f.code;
@@ -1052,12 +1308,15 @@ void fftpim_count_launch(int n) { g_launches += n; }
 
 extern "C" {
 
-int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out) {
+static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool sharded, FftpimPlan** out) {
     if (!p || !out) return fail(Fail{FFTPIM_VALUE, "null argument"});
     *out = nullptr;
     auto t0 = std::chrono::steady_clock::now();
     FftpimPlan* P = new FftpimPlan();
     try {
+        P->world = world;
+        P->rank = rank;
+        P->sharded = sharded;
         P->prob = *p;
         P->device = p->device;
         P->use_graphs = getenv("FFTPIM_NO_GRAPHS") == nullptr;
@@ -1082,6 +1341,81 @@ int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out) {
         fftpim_plan_destroy(P);
         return fail(f);
     }
+}
+
+int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out) { return plan_create_shard(p, 1, 0, false, out); }
+
+int fftpim_nccl_unique_id(void* out, int64_t bytes) {
+    if (!out || bytes < (int64_t)sizeof(ncclUniqueId)) return fail(Fail{FFTPIM_VALUE, "need a 128-byte buffer"});
+    try {
+        ncclUniqueId id;
+        NCK(ncclGetUniqueId(&id));
+        memcpy(out, &id, sizeof(id));
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_group_create(const FftpimProblem* p, int32_t world, int32_t rank, const void* nccl_id,
+                        FftpimGroup** out) {
+    if (!p || !out || world < 1 || rank < 0 || rank >= world) return fail(Fail{FFTPIM_VALUE, "bad group arguments"});
+    *out = nullptr;
+    GroupImpl* G = new GroupImpl();
+    G->world = world;
+    G->rank = rank;
+    G->emulate = nccl_id == nullptr;
+    try {
+        if (G->emulate) {
+            for (int r = 0; r < world; ++r) {
+                FftpimPlan* P = nullptr;
+                int rc = plan_create_shard(p, world, r, true, &P);
+                if (rc) throw Fail{rc, g_last_error};
+                G->shards.push_back(P);
+            }
+        } else {
+            FftpimPlan* P = nullptr;
+            int rc = plan_create_shard(p, world, rank, true, &P);
+            if (rc) throw Fail{rc, g_last_error};
+            G->shards.push_back(P);
+            CK(cudaSetDevice(p->device));
+            ncclUniqueId id;
+            memcpy(&id, nccl_id, sizeof(id));
+            NCK(ncclCommInitRank(&G->comm, world, id, rank));
+        }
+        *out = reinterpret_cast<FftpimGroup*>(G);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        for (auto* P : G->shards) fftpim_plan_destroy(P);
+        if (G->comm) ncclCommDestroy(G->comm);
+        delete G;
+        return fail(f);
+    }
+}
+
+int fftpim_group_evaluate(FftpimGroup* g, const double* q, double* u, void* stream) {
+    if (!g || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    try {
+        group_evaluate(reinterpret_cast<GroupImpl*>(g), q, u, (cudaStream_t)stream);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_group_info(const FftpimGroup* g, int32_t shard, FftpimInfo* info) {
+    const GroupImpl* G = reinterpret_cast<const GroupImpl*>(g);
+    if (!G || !info || shard < 0 || shard >= (int)G->shards.size()) return fail(Fail{FFTPIM_VALUE, "bad shard"});
+    *info = G->shards[shard]->info;
+    return FFTPIM_OK;
+}
+
+void fftpim_group_destroy(FftpimGroup* g) {
+    GroupImpl* G = reinterpret_cast<GroupImpl*>(g);
+    if (!G) return;
+    for (auto* P : G->shards) fftpim_plan_destroy(P);
+    if (G->comm) ncclCommDestroy(G->comm);
+    delete G;
 }
 
 int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts, void* stream) {

@@ -93,10 +93,12 @@ struct EvalArgs {
     const int* obs_start;
     cplx* work;
     cplx* pad_in;               // zero-padded FFT input; only the n^3 corner is written
-    cplx* k1_out;               // K1 target grid, indexed ((x*go1 + y)*go2 + z)
+    cplx* k1_out;               // K1 target grid, indexed (((x-kx0)*go1 + y)*go2 + z)
     int go1, go2;
-    const cplx* interp_grid;    // near potentials on the grid, indexed ((x*gi1 + y)*gi2 + z)
+    int kx0, knx;               // K1 computes planes [kx0, kx0 + knx) (slab shards)
+    const cplx* interp_grid;    // near potentials on the grid, indexed (((x-gx0)*gi1 + y)*gi2 + z)
     int gi1, gi2;
+    int gx0;
     const cplx* khat;
     int64_t n_fft;
     const int64_t* pair_ptr;
@@ -119,6 +121,8 @@ struct EvalArgs {
     cplx* far_qg;
     cplx* far_ug;
     int far_blocks, far_warps;
+    const cplx* far_q;          // sources projected onto the far grid (own range for shards)
+    int64_t far_n;
     int parts;
 };
 void launch_permute_q(const EvalArgs& a, cudaStream_t s);
@@ -127,6 +131,7 @@ void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s);
 void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);
+void launch_axpy(cplx* acc, const cplx* x, int64_t n, cudaStream_t s);   // acc += x
 void launch_observers(const EvalArgs& a, cudaStream_t s);
 
 // ---- pruned column-FFT stages (fft_kernels.cu)

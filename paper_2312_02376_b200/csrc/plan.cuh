@@ -175,6 +175,20 @@ struct FftpimPlan {
     double* h_u = nullptr;
     int64_t h_batch = 0;
 
+    // slab decomposition: shard `rank` of `world` owns near-grid
+    // x-planes [X0, X1), the sorted observers/sources whose stencil starts there
+    // [i0, i1), and FFT columns [C0, C1) for the x transforms
+    int world = 1, rank = 0;
+    bool sharded = false;           // built as a group shard (also for world == 1)
+    int X0 = 0, X1 = 0, n0_loc = 0, halo = 0;
+    int64_t i0 = 0, i1 = 0;
+    int64_t C = 0, C0 = 0, C1 = 0;
+    std::vector<int> plane_start;   // X_r for r = 0..world
+    std::vector<int64_t> col_start; // C_r for r = 0..world
+    cplx* a2a_send = nullptr;       // packed [peer][x_local][column]
+    cplx* a2a_recv = nullptr;       // [x][own column]
+    cplx* far_sum_tmp = nullptr;
+
     // concurrent evaluation schedule (near chain | K4 | far chain)
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr;

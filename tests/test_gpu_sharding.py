@@ -1,0 +1,64 @@
+"""Slab decomposition checked on one GPU: all shards of a group
+emulated in one process (exchanges = device copies) must reproduce the
+single-domain plan and the reference.  The NCCL path runs the same shard code
+with NCCL collectives instead of the copies."""
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fp():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2312_02376_b200 as fp
+    return fp
+
+
+def _objs(fp, c):
+    from paper_2312_02376_b200.workloads import CONFIGS, make_inputs
+    w = CONFIGS[c]
+    pos, q = make_inputs(c)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=w.kshift,
+                               regime=fp.Regime(w.regime))
+    return cfg, fp.TargetBox(w.D), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos), fp.SolverParams(**w.params()), q
+
+
+@pytest.mark.parametrize("c,world", [(1, 2), (1, 4), (2, 2), (2, 3), (2, 8)])
+def test_slab_group_emulated_matches_single_plan(fp, c, world):
+    from paper_2312_02376_b200.sharding import SlabGroup
+    cfg, box, src, obs, prm, q = _objs(fp, c)
+    u1 = fp.build_plan(cfg, box, src, obs, prm).evaluate(q)
+    grp = SlabGroup(cfg, box, src, obs, prm, world=world)
+    u = grp.evaluate(q)
+    assert sum(int(i.n_pairs) for i in grp.infos) == int(golden(f"c{c}_full.npz")["n_pairs"])
+    assert rel_l2(u, u1) <= 1e-13
+    assert rel_l2(u, golden(f"c{c}_full.npz")["u"]) <= 1e-10
+
+
+def test_slab_group_dynamic_3d_small(fp):
+    """3D Helmholtz with a phase shift (the C4 regime) at a small size."""
+    from paper_2312_02376_b200.sharding import SlabGroup
+    rng = np.random.default_rng(11)
+    pos = rng.uniform(0, 1, (3000, 3))
+    q = rng.standard_normal(3000) + 1j * rng.standard_normal(3000)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity.P3D, L=(1, 1, 1), k0=2 * np.pi,
+                               kshift=(0.2 * np.pi, 0.1 * np.pi, 0), regime=fp.Regime.DYNAMIC)
+    prm = fp.SolverParams(near_grid=(16, 16, 16), near_order=4)
+    args = (cfg, fp.TargetBox((1, 1, 1)), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos), prm)
+    u1 = fp.build_plan(*args).evaluate(q)
+    for world in (2, 4):
+        assert rel_l2(SlabGroup(*args, world=world).evaluate(q), u1) <= 1e-13
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_slab_group_nccl_single_rank(fp, c):
+    """The NCCL code path itself (send/recv transposes, all-reduce, halo) with a
+    one-rank communicator on this GPU."""
+    from paper_2312_02376_b200.sharding import SlabGroup, nccl_unique_id
+    cfg, box, src, obs, prm, q = _objs(fp, c)
+    grp = SlabGroup(cfg, box, src, obs, prm, world=1, rank=0, nccl_id=nccl_unique_id())
+    assert rel_l2(grp.evaluate(q), golden(f"c{c}_full.npz")["u"]) <= 1e-10
