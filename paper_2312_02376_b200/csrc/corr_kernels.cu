@@ -183,13 +183,14 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------- K3 + K5c + fix-up
-// Four lanes per observer (lane sub handles x-offsets ia = sub, sub+4, ...);
-// each walks its (ia, ib) rows of the stencil with the z taps contiguous in
-// memory.  The far observer grid (<= 48 KB) is staged in shared memory.  The
+// OBS_LPO lanes per observer (lane sub handles stencil rows (ia, ib) = sub,
+// sub + OBS_LPO, ...), each row's z taps contiguous in memory.  The far observer grid (<= 48 KB) is staged in shared memory.  The
 // quad is reduced with two fixed xor-shuffles, then lane 0 adds the observer's
 // K4 segments.  Single-plane axes: weights past the first tap are zero and the
 // indices are clamped, so those taps add exactly 0.
+#ifndef OBS_LPO
 #define OBS_LPO 4
+#endif
 __device__ __forceinline__ cplx corr_of_row(const EvalArgs& a, int64_t i) {
     const int64_t p0 = a.pair_ptr[i], p1 = a.pair_ptr[i + 1];
     if (p0 == p1) return mk(0.0);
@@ -223,20 +224,16 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
         double wz[W];
 #pragma unroll
         for (int c = 0; c < W; ++c) wz[c] = w[2 * W + c];
-        for (int ia = sub; ia < W; ia += OBS_LPO) {
-            const double wx = w[ia];
-            const int64_t xo = (int64_t)(min(s0 + ia, m0) - a.gx0) * c1;
+        for (int rw = sub; rw < W * W; rw += OBS_LPO) {   // stencil row (ia, ib) per lane
+            const int ia = rw / W, ib = rw - (rw / W) * W;
+            const double wxy = w[ia] * w[W + ib];
+            const cplx* row = a.interp_grid + ((int64_t)(min(s0 + ia, m0) - a.gx0) * c1 + min(s1 + ib, m1)) * c2;
 #pragma unroll
-            for (int ib = 0; ib < W; ++ib) {
-                const double wxy = wx * w[W + ib];
-                const cplx* row = a.interp_grid + (xo + min(s1 + ib, m1)) * c2;
-#pragma unroll
-                for (int ic = 0; ic < W; ++ic) {
-                    const cplx v = row[min(s2 + ic, m2)];
-                    const double wgt = wxy * wz[ic];
-                    ar += wgt * v.re;
-                    ai += wgt * v.im;
-                }
+            for (int ic = 0; ic < W; ++ic) {
+                const cplx v = row[min(s2 + ic, m2)];
+                const double wgt = wxy * wz[ic];
+                ar += wgt * v.re;
+                ai += wgt * v.im;
             }
         }
     }
@@ -247,27 +244,24 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
         double wz[WF];
 #pragma unroll
         for (int c = 0; c < WF; ++c) wz[c] = w[2 * WF + c];
-        for (int ia = sub; ia < WF; ia += OBS_LPO) {
-            const double wx = w[ia];
-            const int xo = min(s0 + ia, nfx - 1) * nfy;
+        for (int rw = sub; rw < WF * WF; rw += OBS_LPO) {
+            const int ia = rw / WF, ib = rw - (rw / WF) * WF;
+            const double wxy = w[ia] * w[WF + ib];
+            const cplx* row = sfar + (min(s0 + ia, nfx - 1) * nfy + min(s1 + ib, nfy - 1)) * nfz;
 #pragma unroll
-            for (int ib = 0; ib < WF; ++ib) {
-                const double wxy = wx * w[WF + ib];
-                const cplx* row = sfar + (xo + min(s1 + ib, nfy - 1)) * nfz;
-#pragma unroll
-                for (int ic = 0; ic < WF; ++ic) {
-                    const cplx v = row[min(s2 + ic, nfz - 1)];
-                    const double wgt = wxy * wz[ic];
-                    ar += wgt * v.re;
-                    ai += wgt * v.im;
-                }
+            for (int ic = 0; ic < WF; ++ic) {
+                const cplx v = row[min(s2 + ic, nfz - 1)];
+                const double wgt = wxy * wz[ic];
+                ar += wgt * v.re;
+                ai += wgt * v.im;
             }
         }
     }
-    ar += __shfl_xor_sync(0xffffffffu, ar, 1);
-    ai += __shfl_xor_sync(0xffffffffu, ai, 1);
-    ar += __shfl_xor_sync(0xffffffffu, ar, 2);
-    ai += __shfl_xor_sync(0xffffffffu, ai, 2);
+#pragma unroll
+    for (int o = 1; o < OBS_LPO; o <<= 1) {   // fixed xor tree over the observer's lanes
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+    }
     if (active && sub == 0) {
         cplx v{ar, ai};
         if (a.parts & FFTPIM_NEAR) v = v + corr_of_row(a, i);

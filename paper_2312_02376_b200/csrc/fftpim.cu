@@ -211,6 +211,16 @@ void sort_points(FftpimPlan* P, const double* d_pos, int64_t n, int* perm, int* 
     CK(cudaFreeAsync(iota, s));
 }
 
+// complex elements per column-FFT block (B columns x L); FFTPIM_FFT_BLOCK tunes it
+int fft_block_elems() {
+    static int v = [] {
+        const char* e = getenv("FFTPIM_FFT_BLOCK");
+        int x = e ? atoi(e) : 1024;
+        return x >= 64 ? x : 1024;
+    }();
+    return v;
+}
+
 // Radix factorisation for the Stockham stages: 4s, a 2, then small primes.
 bool fft_radices(int L, int* radix, int* nrad) {
     int n = 0;
@@ -317,7 +327,7 @@ void setup_fft_pipeline(FftpimPlan* P, const int dims[3], cudaStream_t s) {
     for (int k = 0; k < 5; ++k) {
         FftStage& st = P->stage[k];
         if (!P->stage_on[k]) continue;
-        st.B = std::max(1, std::min(st.nb0, 2048 / st.L));
+        st.B = std::max(1, std::min(st.nb0, fft_block_elems() / st.L));
     }
 }
 
@@ -362,7 +372,7 @@ void setup_fft_pipeline_shard(FftpimPlan* P, const int dims[3], cudaStream_t s) 
     st[2].in = P->a2a_recv; st[2].out = P->a2a_recv; st[2].lin = n0; st[2].lout = n0;
     st[2].in_stride = ncol; st[2].out_stride = ncol; st[2].nb0 = (int)ncol; st[2].in_s0 = 1; st[2].out_s0 = 1;
     st[2].spec = P->khat; st[2].spec_stride = ncol; st[2].spec_s0 = 1;
-    st[2].B = std::max(1, std::min(st[2].nb0, 2048 / st[2].L));
+    st[2].B = std::max(1, std::min(st[2].nb0, fft_block_elems() / st[2].L));
     // S4: y inverse, B -> A
     st[3].in = P->fbufB; st[3].out = P->fbufA; st[3].nb1 = nl;
     // S5: z inverse, A -> qg (own planes, the halo planes follow)
