@@ -174,7 +174,10 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
 void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.n_pairs == 0) return;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
-    const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, 148 * CORR_MINB);
+    // a.corr_blocks caps the grid (the concurrent schedule leaves SMs to the near chain)
+    int cap = 148 * CORR_MINB;
+    if (a.corr_blocks > 0) cap = std::min(cap, a.corr_blocks);
+    const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, cap);
     if (a.coef_r)
         k_corr_tiles<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
     else

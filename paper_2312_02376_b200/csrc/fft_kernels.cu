@@ -192,9 +192,137 @@ __global__ void __launch_bounds__(256) k_fft_stage(FftStage st) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Power-of-two lengths with B = 1024 / L columns per block: the same Stockham
+// radix-4 (+ one radix-2) algorithm with every index, pass span and twiddle
+// offset known at compile time, so each thread executes straight-line code.
+template <int L, int R, int P>
+__device__ __forceinline__ void p2_pass(const cplx* __restrict__ x, cplx* __restrict__ y, const cplx* __restrict__ twp,
+                                        int sign) {
+    constexpr int B = 1024 / L, M = L / R, LP = L + 1;
+    constexpr int NB = B * M;   // butterflies in this pass
+#pragma unroll
+    for (int rep = 0; rep < (NB + 255) / 256; ++rep) {
+        const int idx = threadIdx.x + 256 * rep;
+        if (NB % 256 != 0 && idx >= NB) break;
+        const int b = idx / M, j = idx % M;
+        const int k = j % P, jp = j / P;
+        const cplx* xb = x + b * LP;
+        cplx* yb = y + b * LP;
+        const int base = jp * P * R + k;
+        if (R == 4) {
+            cplx a0 = xb[swz(j, L)], a1 = xb[swz(j + M, L)], a2 = xb[swz(j + 2 * M, L)], a3 = xb[swz(j + 3 * M, L)];
+            if (P > 1) {
+                a1 = a1 * twid(twp, k, sign);
+                a2 = a2 * twid(twp, P + k, sign);
+                a3 = a3 * twid(twp, 2 * P + k, sign);
+            }
+            const cplx t0 = a0 + a2, t1 = a0 - a2, t2 = a1 + a3, t3 = mul_si(a1 - a3, sign);
+            yb[swz(base, L)] = t0 + t2;
+            yb[swz(base + P, L)] = t1 + t3;
+            yb[swz(base + 2 * P, L)] = t0 - t2;
+            yb[swz(base + 3 * P, L)] = t1 - t3;
+        } else {
+            cplx a0 = xb[swz(j, L)], a1 = xb[swz(j + M, L)];
+            if (P > 1) a1 = a1 * twid(twp, k, sign);
+            yb[swz(base, L)] = a0 + a1;
+            yb[swz(base + P, L)] = a0 - a1;
+        }
+    }
+}
+
+// passes while P < L: radix 4 while at least 4 remain, then radix 2
+template <int L, int P, int OFF>
+__device__ __forceinline__ cplx* p2_passes(cplx* x, cplx* y, const cplx* twp, int sign) {
+    if constexpr (P >= L) {
+        return x;
+    } else {
+        constexpr int R = (L / P >= 4) ? 4 : 2;
+        p2_pass<L, R, P>(x, y, twp + OFF, sign);
+        __syncthreads();
+        return p2_passes<L, P * R, OFF + (R - 1) * P>(y, x, twp, sign);
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) k_fft_stage_p2(FftStage st) {
+    constexpr int B = 1024 / L, LP = L + 1;
+    extern __shared__ cplx sm[];
+    cplx* x = sm;
+    cplx* y = sm + B * LP;
+    cplx* twp = sm + 2 * B * LP;
+    for (int t = threadIdx.x; t < st.ntwp; t += 256) twp[t] = st.twp[t];
+    const int c0 = blockIdx.x * B;
+    const int nb = min(B, st.nb0 - c0);
+    const int64_t in_base = (int64_t)blockIdx.y * st.in_s1 + (int64_t)c0 * st.in_s0;
+    const int64_t out_base = (int64_t)blockIdx.y * st.out_s1 + (int64_t)c0 * st.out_s0;
+    if (st.in_stride == 1) {
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < B * L; idx += 256) {
+            const int b = idx / L, i = idx % L;
+            x[b * LP + swz(i, L)] = (b < nb && i < st.lin) ? st.in[in_base + b * st.in_s0 + i] : mk(0.0);
+        }
+    } else {
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < B * L; idx += 256) {
+            const int i = idx / B, b = idx % B;
+            x[b * LP + swz(i, L)] = (b < nb && i < st.lin) ? st.in[in_base + b * st.in_s0 + (int64_t)i * st.in_stride] : mk(0.0);
+        }
+    }
+    __syncthreads();
+    cplx* r;
+    if (st.spec) {
+        r = p2_passes<L, 1, 0>(x, y, twp, -1);
+        const int64_t sp_base = (int64_t)blockIdx.y * st.spec_s1 + (int64_t)c0 * st.spec_s0;
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < B * L; idx += 256) {
+            const int k = idx / B, b = idx % B;
+            if (b < nb) r[b * LP + swz(k, L)] = r[b * LP + swz(k, L)] * st.spec[sp_base + b * st.spec_s0 + (int64_t)k * st.spec_stride];
+        }
+        __syncthreads();
+        r = p2_passes<L, 1, 0>(r, r == x ? y : x, twp, +1);
+    } else {
+        r = p2_passes<L, 1, 0>(x, y, twp, st.sign);
+    }
+    if (st.out_stride == 1) {
+        for (int idx = threadIdx.x; idx < B * st.lout; idx += 256) {
+            const int b = idx / st.lout, i = idx - b * st.lout;
+            if (b < nb) st.out[out_base + b * st.out_s0 + i] = r[b * LP + swz(i, L)];
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < B * st.lout; idx += 256) {
+            const int i = idx / B, b = idx % B;
+            if (b < nb) st.out[out_base + b * st.out_s0 + (int64_t)i * st.out_stride] = r[b * LP + swz(i, L)];
+        }
+    }
+}
+
+template <int L>
+static bool p2_launch(const FftStage& st, cudaStream_t s) {
+    if (st.L != L || st.B != 1024 / L) return false;
+    const size_t smem = (size_t)(2 * (1024 / L) * (L + 1) + st.ntwp) * sizeof(cplx);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_fft_stage_p2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 4096);
+        configured = true;
+    }
+    dim3 grid((st.nb0 + st.B - 1) / st.B, st.nb1);
+    k_fft_stage_p2<L><<<grid, 256, smem, s>>>(st);
+    return true;
+}
+
+static bool launch_fft_stage_p2(const FftStage& st, cudaStream_t s) {
+    return p2_launch<16>(st, s) || p2_launch<32>(st, s) || p2_launch<64>(st, s) || p2_launch<128>(st, s) ||
+           p2_launch<256>(st, s) || p2_launch<512>(st, s) || p2_launch<1024>(st, s);
+}
+
 size_t fft_stage_smem(const FftStage& st) { return (size_t)(2 * st.B * (st.L + 1) + st.L + st.ntwp) * sizeof(cplx); }
 
 void launch_fft_stage(const FftStage& st, cudaStream_t s) {
+    if (launch_fft_stage_p2(st, s)) {
+        fftpim_count_launch();
+        return;
+    }
     const size_t smem = fft_stage_smem(st);
     static size_t configured = 48 * 1024;
     if (smem > configured) {

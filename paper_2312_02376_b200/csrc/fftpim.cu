@@ -1050,7 +1050,17 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
             }
             CK(cudaEventRecord(P->ev_join[0], sn));
             CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
-            launch_corr_tiles(a, sc);
+            {
+                // K4 streams HBM on part of the chip while the latency-bound
+                // near chain runs on the rest (FFTPIM_CORR_BLOCKS tunes the split)
+                static const int cb = [] {
+                    const char* e = getenv("FFTPIM_CORR_BLOCKS");
+                    return e ? atoi(e) : 2 * 148;
+                }();
+                EvalArgs ac = a;
+                ac.corr_blocks = cb;
+                launch_corr_tiles(ac, sc);
+            }
             CK(cudaEventRecord(P->ev_join[1], sc));
             CK(cudaStreamWaitEvent(s, P->ev_join[0], 0));
             CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));

@@ -110,6 +110,7 @@ struct EvalArgs {
     const int64_t* seg_base;    // per CORR_TILE tile: global index of its first segment
     const int64_t* seg_first;   // per observer: global index of its first segment
     cplx* seg_val;              // (row, tile) segment sums
+    int corr_blocks;            // K4 grid cap (0 = whole chip)
     // far
     StencilGeom fs, fo;
     const double* src_fw;
