@@ -226,8 +226,139 @@ static void k1_tiled_launch(const EvalArgs& a, cudaStream_t s) {
     k_near_project_tiled<W><<<grid, K1_TX * K1_TY * K1_TZ, smem, s>>>(a);
 }
 
+// Tap-major K1 (point-centric, deterministic): a block owns a TX x TY x TZ tile
+// of stencil-start cells, one thread per cell holding its first points' stencil
+// weights in registers.  For each of the (order+1)^3 taps in a fixed order every
+// thread adds its cell's contribution to node cell+tap of the block's extended
+// node tile in shared memory -- distinct cells hit distinct nodes for a fixed
+// tap, and a barrier separates taps, so there are no races and no atomics.  The
+// overlapping extended tiles are then summed per node in fixed block order.
+#define K1T_TX 4
+#define K1T_TY 4
+#define K1T_TZ 16
+#define K1T_REG 2
+template <int W>
+struct K1Taps {
+    static constexpr int EX = K1T_TX + W - 1, EY = K1T_TY + W - 1, EZ = K1T_TZ + W - 1;
+    static constexpr int NODES = EX * EY * EZ;
+};
+
+template <int W>
+__global__ void __launch_bounds__(K1T_TX * K1T_TY * K1T_TZ) k_near_project_taps(EvalArgs a) {
+    using T = K1Taps<W>;
+    __shared__ cplx tile[T::NODES];
+    const StencilGeom& g = a.g;
+    for (int n = threadIdx.x; n < T::NODES; n += blockDim.x) tile[n] = mk(0.0);
+    const int lx = threadIdx.x / (K1T_TY * K1T_TZ), ly = (threadIdx.x / K1T_TZ) % K1T_TY, lz = threadIdx.x % K1T_TZ;
+    const int cx = a.kx0 - (W - 1) + blockIdx.x * K1T_TX + lx;   // start cells of the slab's reach
+    const int cy = blockIdx.y * K1T_TY + ly, cz = blockIdx.z * K1T_TZ + lz;
+    int p0 = 0, p1 = 0;
+    if (cx >= 0 && cx < g.nc[0] && cy < g.nc[1] && cz < g.nc[2]) {
+        const int k = (cx * g.nc[1] + cy) * g.nc[2] + cz;
+        p0 = a.cell_start[k];
+        p1 = a.cell_start[k + 1];
+    }
+    double w[K1T_REG][3 * W];
+    cplx qv[K1T_REG];
+    const int nreg = min(p1 - p0, K1T_REG);
+#pragma unroll
+    for (int r = 0; r < K1T_REG; ++r) {
+        if (r < nreg) {
+            const double* src = a.src_w + (int64_t)(p0 + r) * 3 * W;
+#pragma unroll
+            for (int j = 0; j < 3 * W; ++j) w[r][j] = src[j];
+            qv[r] = a.q_sorted[p0 + r];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ia = 0; ia < W; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < W; ++ib)
+#pragma unroll
+            for (int ic = 0; ic < W; ++ic) {
+                if (p1 > p0) {
+                    cplx acc = mk(0.0);
+#pragma unroll
+                    for (int r = 0; r < K1T_REG; ++r)
+                        if (r < nreg) {
+                            const double wgt = (w[r][ia] * w[r][W + ib]) * w[r][2 * W + ic];
+                            acc.re += wgt * qv[r].re;
+                            acc.im += wgt * qv[r].im;
+                        }
+                    for (int p = p0 + K1T_REG; p < p1; ++p) {   // crowded cells: from L1/L2
+                        const double* wp = a.src_w + (int64_t)p * 3 * W;
+                        const double wgt = (wp[ia] * wp[W + ib]) * wp[2 * W + ic];
+                        const cplx qp = a.q_sorted[p];
+                        acc.re += wgt * qp.re;
+                        acc.im += wgt * qp.im;
+                    }
+                    cplx& dst = tile[((lx + ia) * T::EY + (ly + ib)) * T::EZ + (lz + ic)];
+                    dst = dst + acc;
+                }
+                __syncthreads();
+            }
+    cplx* out = a.k1_scratch + ((int64_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * T::NODES;
+    for (int n = threadIdx.x; n < T::NODES; n += blockDim.x) out[n] = tile[n];
+}
+
+// node (x, y, z) = sum of the extended tiles covering it, blocks in fixed order
+template <int W>
+__global__ void __launch_bounds__(256) k_near_project_combine(EvalArgs a, int gx, int gy, int gz) {
+    using T = K1Taps<W>;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const StencilGeom& g = a.g;
+    if (t >= (int64_t)a.knx * g.n[1] * g.n[2]) return;
+    const int z = (int)(t % g.n[2]), y = (int)((t / g.n[2]) % g.n[1]), xl = (int)(t / ((int64_t)g.n[1] * g.n[2]));
+    // block bx covers (slab-local, shifted by order) x in [bx*TX, bx*TX + EX)
+    const int xs = xl + (W - 1);
+    cplx acc = mk(0.0);
+    for (int bx = max(0, (xs - T::EX + K1T_TX) / K1T_TX); bx <= min(gx - 1, xs / K1T_TX); ++bx) {
+        const int ox = xs - bx * K1T_TX;
+        if (ox >= T::EX) continue;
+        for (int by = max(0, (y - T::EY + K1T_TY) / K1T_TY); by <= min(gy - 1, y / K1T_TY); ++by) {
+            const int oy = y - by * K1T_TY;
+            if (oy >= T::EY) continue;
+            for (int bz = max(0, (z - T::EZ + K1T_TZ) / K1T_TZ); bz <= min(gz - 1, z / K1T_TZ); ++bz) {
+                const int oz = z - bz * K1T_TZ;
+                if (oz >= T::EZ) continue;
+                acc = acc + a.k1_scratch[((int64_t)(bz * gy + by) * gx + bx) * T::NODES + (ox * T::EY + oy) * T::EZ + oz];
+            }
+        }
+    }
+    a.k1_out[((int64_t)xl * a.go1 + y) * a.go2 + z] = acc;
+}
+
+template <int W>
+static void k1_taps_launch(const EvalArgs& a, cudaStream_t s) {
+    // cells reaching the slab's planes: [kx0 - order, kx0 + knx) in x
+    const int gx = (a.knx + W - 1 + K1T_TX - 1) / K1T_TX;
+    const int gy = (a.g.nc[1] + K1T_TY - 1) / K1T_TY, gz = (a.g.nc[2] + K1T_TZ - 1) / K1T_TZ;
+    k_near_project_taps<W><<<dim3(gx, gy, gz), K1T_TX * K1T_TY * K1T_TZ, 0, s>>>(a);
+    const int64_t nodes = (int64_t)a.knx * a.g.n[1] * a.g.n[2];
+    k_near_project_combine<W><<<nblk(nodes, 256), 256, 0, s>>>(a, gx, gy, gz);
+}
+
+int64_t k1_scratch_elems(const StencilGeom& g, int knx) {
+    const int W = g.order + 1;
+    const int gx = (knx + W - 1 + K1T_TX - 1) / K1T_TX;
+    const int gy = (g.nc[1] + K1T_TY - 1) / K1T_TY, gz = (g.nc[2] + K1T_TZ - 1) / K1T_TZ;
+    const int64_t nodes = (int64_t)(K1T_TX + W - 1) * (K1T_TY + W - 1) * (K1T_TZ + W - 1);
+    return (int64_t)gx * gy * gz * nodes;
+}
+
 bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s) {
     if (a.g.n[0] < 2 || a.g.n[1] < 2 || a.g.n[2] < 2) return false;   // single-plane axes: global path
+    if (a.k1_scratch) {
+        switch (a.g.order + 1) {
+            case 3: k1_taps_launch<3>(a, s); break;
+            case 4: k1_taps_launch<4>(a, s); break;
+            case 5: k1_taps_launch<5>(a, s); break;
+            default: return false;
+        }
+        fftpim_count_launch(2);
+        return true;
+    }
     switch (a.g.order + 1) {
         case 3: k1_tiled_launch<3>(a, s); break;
         case 4: k1_tiled_launch<4>(a, s); break;

@@ -580,6 +580,17 @@ void build(FftpimPlan* P) {
         CK(cudaMemsetAsync(P->pad_in, 0, sizeof(cplx) * P->n_fft, s));   // padding stays zero: out-of-place forward FFT
     }
     P->q_sorted = dalloc<cplx>(P, N);
+    {
+        // tap-major K1 (3 active axes, orders 2..4) pays off for crowded cells
+        // (clustered sources, C3: >= 1 point per stencil cell on average); sparse
+        // grids keep the gather K1.  FFTPIM_K1=taps|gather overrides.
+        const char* e = getenv("FFTPIM_K1");
+        const double density = (double)N / (double)prod3(P->near_g.nc);
+        bool taps = density >= 1.0;
+        if (e) taps = std::string(e) == "taps";
+        if (taps && dims[0] > 1 && dims[1] > 1 && dims[2] > 1 && pr.near_order >= 2 && pr.near_order <= 4)
+            P->k1_scratch = dalloc<cplx>(P, k1_scratch_elems(P->near_g, P->n0_loc));
+    }
 
     // ---- correction pairs (nearzone.py:245-256, 303-487)
     PairGeom& pg = P->pg;
@@ -970,6 +981,7 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.far_warps = P->far_warps;
     a.far_q = P->q_sorted;
     a.far_n = P->N;
+    a.k1_scratch = P->k1_scratch;
     a.kx0 = 0;
     a.knx = P->near_g.n[0];
     a.gx0 = 0;

@@ -96,6 +96,7 @@ struct EvalArgs {
     cplx* k1_out;               // K1 target grid, indexed (((x-kx0)*go1 + y)*go2 + z)
     int go1, go2;
     int kx0, knx;               // K1 computes planes [kx0, kx0 + knx) (slab shards)
+    cplx* k1_scratch;           // tap-major K1 block tiles (null: gather K1)
     const cplx* interp_grid;    // near potentials on the grid, indexed (((x-gx0)*gi1 + y)*gi2 + z)
     int gi1, gi2;
     int gx0;
@@ -127,6 +128,7 @@ struct EvalArgs {
     int parts;
 };
 void launch_permute_q(const EvalArgs& a, cudaStream_t s);
+int64_t k1_scratch_elems(const StencilGeom& g, int knx);
 void launch_near_project(const EvalArgs& a, cudaStream_t s);
 void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s);
 void launch_far_project(const EvalArgs& a, cudaStream_t s);

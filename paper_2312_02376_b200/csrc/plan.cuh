@@ -129,6 +129,7 @@ struct FftpimPlan {
     cplx* pad_in = nullptr;       // zero-padded projection (corner written each eval)
     cufftHandle fft_plan = 0;
     cplx* q_sorted = nullptr;     // (N) charges permuted to sorted order
+    cplx* k1_scratch = nullptr;   // tap-major K1 extended block tiles
 
     // corrections (CSR over sorted observers)
     int64_t* pair_ptr = nullptr;  // (M+1)
