@@ -218,6 +218,13 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
     const bool active = i < a.M;
     const int64_t ii = active ? i : a.M - 1;
     double ar = 0.0, ai = 0.0;
+    if ((a.parts & FFTPIM_NEAR) && active && sub == OBS_LPO - 1) {
+        // the observer's K4 segments, fetched by the last lane up front so the
+        // dependent pointer chain overlaps the interpolation gathers
+        const cplx c = corr_of_row(a, i);
+        ar = c.re;
+        ai = c.im;
+    }
     if (a.parts & FFTPIM_NEAR) {
         const double* w = a.obs_w + ii * 3 * W;
         const int* st = a.obs_start + 3 * ii;
@@ -265,11 +272,7 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
         ar += __shfl_xor_sync(0xffffffffu, ar, o);
         ai += __shfl_xor_sync(0xffffffffu, ai, o);
     }
-    if (active && sub == 0) {
-        cplx v{ar, ai};
-        if (a.parts & FFTPIM_NEAR) v = v + corr_of_row(a, i);
-        a.u[a.obs_perm[i]] = v;
-    }
+    if (active && sub == 0) a.u[a.obs_perm[i]] = cplx{ar, ai};
 }
 
 template <int W>
