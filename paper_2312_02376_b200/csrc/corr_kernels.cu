@@ -186,11 +186,13 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------- K3 + K5c + fix-up
-// OBS_LPO lanes per observer (lane sub handles stencil rows (ia, ib) = sub,
-// sub + OBS_LPO, ...), each row's z taps contiguous in memory.  The far observer grid (<= 48 KB) is staged in shared memory.  The
-// quad is reduced with two fixed xor-shuffles, then lane 0 adds the observer's
-// K4 segments.  Single-plane axes: weights past the first tap are zero and the
-// indices are clamped, so those taps add exactly 0.
+// OBS_LPO lanes per observer; every lane walks all W*W stencil rows (ia, ib) and
+// takes the z taps sub, sub + OBS_LPO, ... of each, so one warp load reads one
+// contiguous row per observer.  The far observer grid (<= 48 KB) is staged in
+// shared memory.  The last lane fetches the observer's K4 segments, the lanes
+// are reduced with a fixed xor tree and lane 0 stores.  Single-plane axes:
+// weights past the first tap are zero and the indices are clamped, so those
+// taps add exactly 0.
 #ifndef OBS_LPO
 #define OBS_LPO 4
 #endif
@@ -226,24 +228,42 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
         ai = c.im;
     }
     if (a.parts & FFTPIM_NEAR) {
+        // lanes split each stencil row along z (lane sub takes z taps sub, sub+4, ...)
+        // so the observer's lanes read one contiguous row per load
         const double* w = a.obs_w + ii * 3 * W;
         const int* st = a.obs_start + 3 * ii;
         const int c1 = a.gi1, c2 = a.gi2;
         const int m0 = a.g.n[0] - 1, m1 = a.g.n[1] - 1, m2 = a.g.n[2] - 1;
         const int s0 = st[0], s1 = st[1], s2 = st[2];
-        double wz[W];
+        double wx[W], wy[W];
 #pragma unroll
-        for (int c = 0; c < W; ++c) wz[c] = w[2 * W + c];
-        for (int rw = sub; rw < W * W; rw += OBS_LPO) {   // stencil row (ia, ib) per lane
-            const int ia = rw / W, ib = rw - (rw / W) * W;
-            const double wxy = w[ia] * w[W + ib];
-            const cplx* row = a.interp_grid + ((int64_t)(min(s0 + ia, m0) - a.gx0) * c1 + min(s1 + ib, m1)) * c2;
+        for (int c = 0; c < W; ++c) {
+            wx[c] = w[c];
+            wy[c] = w[W + c];
+        }
+        constexpr int ZT = (W + OBS_LPO - 1) / OBS_LPO;
+        double wz[ZT];
+        int oz[ZT];
 #pragma unroll
-            for (int ic = 0; ic < W; ++ic) {
-                const cplx v = row[min(s2 + ic, m2)];
-                const double wgt = wxy * wz[ic];
-                ar += wgt * v.re;
-                ai += wgt * v.im;
+        for (int t = 0; t < ZT; ++t) {
+            const int ic = sub + t * OBS_LPO;
+            wz[t] = ic < W ? w[2 * W + ic] : 0.0;
+            oz[t] = min(s2 + min(ic, W - 1), m2);
+        }
+#pragma unroll
+        for (int ia = 0; ia < W; ++ia) {
+            const cplx* plane = a.interp_grid + (int64_t)(min(s0 + ia, m0) - a.gx0) * c1 * c2;
+#pragma unroll
+            for (int ib = 0; ib < W; ++ib) {
+                const double wxy = wx[ia] * wy[ib];
+                const cplx* row = plane + (int64_t)min(s1 + ib, m1) * c2;
+#pragma unroll
+                for (int t = 0; t < ZT; ++t) {
+                    const cplx v = row[oz[t]];
+                    const double wgt = wxy * wz[t];
+                    ar += wgt * v.re;
+                    ai += wgt * v.im;
+                }
             }
         }
     }
@@ -251,19 +271,34 @@ __global__ void __launch_bounds__(256) k_observers(EvalArgs a) {
         const double* w = a.obs_fw + ii * 3 * WF;
         const int* st = a.obs_fstart + 3 * ii;
         const int s0 = st[0], s1 = st[1], s2 = st[2];
-        double wz[WF];
+        double wx[WF], wy[WF];
 #pragma unroll
-        for (int c = 0; c < WF; ++c) wz[c] = w[2 * WF + c];
-        for (int rw = sub; rw < WF * WF; rw += OBS_LPO) {
-            const int ia = rw / WF, ib = rw - (rw / WF) * WF;
-            const double wxy = w[ia] * w[WF + ib];
-            const cplx* row = sfar + (min(s0 + ia, nfx - 1) * nfy + min(s1 + ib, nfy - 1)) * nfz;
+        for (int c = 0; c < WF; ++c) {
+            wx[c] = w[c];
+            wy[c] = w[WF + c];
+        }
+        constexpr int ZT = (WF + OBS_LPO - 1) / OBS_LPO;
+        double wz[ZT];
+        int oz[ZT];
 #pragma unroll
-            for (int ic = 0; ic < WF; ++ic) {
-                const cplx v = row[min(s2 + ic, nfz - 1)];
-                const double wgt = wxy * wz[ic];
-                ar += wgt * v.re;
-                ai += wgt * v.im;
+        for (int t = 0; t < ZT; ++t) {
+            const int ic = sub + t * OBS_LPO;
+            wz[t] = ic < WF ? w[2 * WF + ic] : 0.0;
+            oz[t] = min(s2 + min(ic, WF - 1), nfz - 1);
+        }
+#pragma unroll
+        for (int ia = 0; ia < WF; ++ia) {
+#pragma unroll
+            for (int ib = 0; ib < WF; ++ib) {
+                const double wxy = wx[ia] * wy[ib];
+                const cplx* row = sfar + (min(s0 + ia, nfx - 1) * nfy + min(s1 + ib, nfy - 1)) * nfz;
+#pragma unroll
+                for (int t = 0; t < ZT; ++t) {
+                    const cplx v = row[oz[t]];
+                    const double wgt = wxy * wz[t];
+                    ar += wgt * v.re;
+                    ai += wgt * v.im;
+                }
             }
         }
     }

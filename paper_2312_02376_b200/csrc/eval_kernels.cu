@@ -8,6 +8,8 @@
 //       interpolation in one warp per observer (grids.py:183-188, nearzone.py:506-524,
 //       farzone.py:159)
 // Every reduction has a fixed order: results are bitwise reproducible run to run.
+#include <cub/block/block_radix_sort.cuh>
+
 #include "geom.cuh"
 #include "kernels.h"
 
@@ -80,7 +82,154 @@ __global__ void __launch_bounds__(256) k_near_project(EvalArgs a) {
 
 bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------- K1 as a fixed sparse operator
+// The projection weights depend only on the source positions, so the plan can
+// hold K1 as a sliced-ELL matrix over the grid nodes (rows).  Within each window
+// of K1E_WIN consecutive rows the rows are ordered by decreasing length
+// (k1_row), so the 32 rows of a slice have nearly equal lengths; entry k of slot
+// t (= sorted position) lives at off[t / 32] + 32 k + t % 32 (int32 source
+// index, fp64 weight product).  Each row lists its points in the gather K1's
+// order (ia, ib, ascending point) with the same weight expression, so the
+// evaluation sums are bit-identical to k_near_project's.
+#define K1E_WIN 256
+template <int W, bool FILL>
+__global__ void __launch_bounds__(256) k_k1_rows(EvalArgs a, int* cnt, const int* row_of, const int64_t* off,
+                                                 const int* remap, int* idx, double* wgt) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const StencilGeom& g = a.g;
+    if (t >= (int64_t)a.knx * g.n[1] * g.n[2]) return;
+    const int64_t r = FILL ? row_of[t] : t;
+    const int z = (int)(r % g.n[2]), y = (int)((r / g.n[2]) % g.n[1]),
+              x = (int)(r / ((int64_t)g.n[1] * g.n[2])) + a.kx0;
+    const int64_t base = FILL ? off[t >> 5] + (t & 31) : 0;
+    int n = 0;
+    const int wx = g.w[0], wy = g.w[1], wz = g.w[2];
+    const int zlo = max(z - (wz - 1), 0), zhi = min(z, g.nc[2] - 1);
+    for (int ia = 0; ia < wx; ++ia) {
+        const int sx = x - ia;
+        if (sx < 0 || sx >= g.nc[0] || zlo > zhi) continue;
+        for (int ib = 0; ib < wy; ++ib) {
+            const int sy = y - ib;
+            if (sy < 0 || sy >= g.nc[1]) continue;
+            const int k0 = (sx * g.nc[1] + sy) * g.nc[2];
+            const int p0 = a.cell_start[k0 + zlo], p1 = a.cell_start[k0 + zhi + 1];
+            if (FILL) {
+                for (int p = p0; p < p1; ++p) {
+                    const double* w = a.src_w + (int64_t)p * 3 * W;
+                    const int ic = z - a.src_start[3 * (int64_t)p + 2];
+                    idx[base + 32 * (int64_t)n] = remap ? remap[p] : p;
+                    wgt[base + 32 * (int64_t)n] = (w[ia] * w[W + ib]) * w[2 * W + ic];
+                    ++n;
+                }
+            } else {
+                n += p1 - p0;
+            }
+        }
+    }
+    if (!FILL) cnt[t] = n;
+}
+
+// per window: rows by decreasing length (stable), lengths moved along
+__global__ void __launch_bounds__(K1E_WIN) k_k1_window_sort(const int* __restrict__ cnt_row, int64_t rows,
+                                                           int* cnt_sorted, int* row_of) {
+    using Sort = cub::BlockRadixSort<int, K1E_WIN, 1, int>;
+    __shared__ typename Sort::TempStorage tmp;
+    const int64_t r = (int64_t)blockIdx.x * K1E_WIN + threadIdx.x;
+    int key[1] = {r < rows ? cnt_row[r] : -1};
+    int val[1] = {(int)r};
+    Sort(tmp).SortDescending(key, val);
+    const int64_t o = (int64_t)blockIdx.x * K1E_WIN + threadIdx.x;
+    if (o < rows) {
+        cnt_sorted[o] = key[0];
+        row_of[o] = val[0];
+    }
+}
+
+// 32 * (longest row of the slice), slice s; entry nslices is 0 (exclusive scan)
+__global__ void k_k1_slice_slots(const int* __restrict__ cnt, int64_t rows, int64_t nslices, int64_t* slots) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s > nslices) return;
+    int m = 0;
+    if (s < nslices)
+        for (int l = 0; l < 32 && 32 * s + l < rows; ++l) m = max(m, cnt[32 * s + l]);
+    slots[s] = 32 * (int64_t)m;
+}
+
+void launch_k1_count(const EvalArgs& a, int* cnt_row, int* cnt_sorted, int* row_of, int64_t* slots,
+                     cudaStream_t s) {
+    const int64_t rows = (int64_t)a.knx * a.g.n[1] * a.g.n[2];
+    const int b = nblk(rows, 256);
+    switch (a.g.order + 1) {
+        case 2: k_k1_rows<2, false><<<b, 256, 0, s>>>(a, cnt_row, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 3: k_k1_rows<3, false><<<b, 256, 0, s>>>(a, cnt_row, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 4: k_k1_rows<4, false><<<b, 256, 0, s>>>(a, cnt_row, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 5: k_k1_rows<5, false><<<b, 256, 0, s>>>(a, cnt_row, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 6: k_k1_rows<6, false><<<b, 256, 0, s>>>(a, cnt_row, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        default: k_k1_rows<7, false><<<b, 256, 0, s>>>(a, cnt_row, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+    }
+    k_k1_window_sort<<<nblk(rows, K1E_WIN), K1E_WIN, 0, s>>>(cnt_row, rows, cnt_sorted, row_of);
+    const int64_t nsl = (rows + 31) / 32;
+    k_k1_slice_slots<<<nblk(nsl + 1, 256), 256, 0, s>>>(cnt_sorted, rows, nsl, slots);
+    fftpim_count_launch(3);
+}
+
+void launch_k1_fill(const EvalArgs& a, const int* row_of, const int64_t* off, const int* remap, int* idx,
+                    double* wgt, cudaStream_t s) {
+    const int b = nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], 256);
+    switch (a.g.order + 1) {
+        case 2: k_k1_rows<2, true><<<b, 256, 0, s>>>(a, nullptr, row_of, off, remap, idx, wgt); break;
+        case 3: k_k1_rows<3, true><<<b, 256, 0, s>>>(a, nullptr, row_of, off, remap, idx, wgt); break;
+        case 4: k_k1_rows<4, true><<<b, 256, 0, s>>>(a, nullptr, row_of, off, remap, idx, wgt); break;
+        case 5: k_k1_rows<5, true><<<b, 256, 0, s>>>(a, nullptr, row_of, off, remap, idx, wgt); break;
+        case 6: k_k1_rows<6, true><<<b, 256, 0, s>>>(a, nullptr, row_of, off, remap, idx, wgt); break;
+        default: k_k1_rows<7, true><<<b, 256, 0, s>>>(a, nullptr, row_of, off, remap, idx, wgt); break;
+    }
+    fftpim_count_launch();
+}
+
+// one thread per slot (grid node): the row's entries eight at a time, all index
+// and weight loads of a chunk issued before its gathers
+#define K1E_U 8
+__global__ void __launch_bounds__(256) k_k1_spmv(EvalArgs a) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int n1 = a.g.n[1], n2 = a.g.n[2];
+    if (t >= (int64_t)a.knx * n1 * n2) return;
+    const int n = a.k1_cnt[t];
+    const int64_t r = a.k1_row[t];
+    const int64_t base = a.k1_off[t >> 5] + (t & 31);
+    const int* __restrict__ ix = a.k1_idx + base;
+    const double* __restrict__ wt = a.k1_wgt + base;
+    const cplx* __restrict__ q = a.k1_q;
+    double ar = 0.0, ai = 0.0;
+    for (int k = 0; k < n; k += K1E_U) {
+        int p[K1E_U];
+        double w[K1E_U];
+#pragma unroll
+        for (int j = 0; j < K1E_U; ++j) {
+            const bool ok = k + j < n;
+            p[j] = ok ? __ldcs(ix + 32 * (int64_t)(k + j)) : 0;
+            w[j] = ok ? __ldcs(wt + 32 * (int64_t)(k + j)) : 0.0;
+        }
+        cplx v[K1E_U];
+#pragma unroll
+        for (int j = 0; j < K1E_U; ++j) v[j] = k + j < n ? q[p[j]] : mk(0.0);
+#pragma unroll
+        for (int j = 0; j < K1E_U; ++j)
+            if (k + j < n) {
+                ar += w[j] * v[j].re;
+                ai += w[j] * v[j].im;
+            }
+    }
+    const int z = (int)(r % n2), y = (int)((r / n2) % n1), xl = (int)(r / ((int64_t)n1 * n2));
+    a.k1_out[((int64_t)xl * a.go1 + y) * a.go2 + z] = cplx{ar, ai};
+}
+
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {
+    if (a.k1_off) {
+        k_k1_spmv<<<nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], 256), 256, 0, s>>>(a);
+        fftpim_count_launch();
+        return;
+    }
     if (launch_near_project_tiled(a, s)) return;
     const int W = a.g.order + 1;
     const int b = nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], 256);

@@ -2,6 +2,7 @@
 // evaluation, operand export.  The host code here only sets up scalars and
 // launches kernels; every O(N) or O(pairs) step runs on the GPU.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -379,6 +380,8 @@ void setup_fft_pipeline_shard(FftpimPlan* P, const int dims[3], cudaStream_t s) 
     st[4].in = P->fbufA; st[4].out = P->qg; st[4].nb1 = nl;
     (void)L0;
 }
+
+EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts);
 
 void build(FftpimPlan* P) {
     const FftpimProblem& pr = P->prob;
@@ -844,6 +847,73 @@ void build(FftpimPlan* P) {
     dfree(P, aug_orig);
     dfree(P, aug_code);
 
+    // ---- K1 as a sliced-ELL operator (eval_kernels.cu) when its entries fit in
+    // half the free memory and no row is long enough to serialise a warp
+    // (clustered sources keep the computed K1); FFTPIM_K1=gather|taps|ell overrides
+    {
+        const char* e = getenv("FFTPIM_K1");
+        if (!e || std::string(e) == "ell") {
+            EvalArgs a = eval_args(P, nullptr, nullptr, FFTPIM_NEAR);
+            const int64_t rows = (int64_t)a.knx * dims[1] * dims[2];
+            const int64_t nsl = (rows + 31) / 32;
+            int* cnt_row = dalloc<int>(P, rows);
+            int* cnt = dalloc<int>(P, rows);
+            int* row_of = dalloc<int>(P, rows);
+            int64_t* off = dalloc<int64_t>(P, nsl + 1);
+            int64_t* slots = dalloc<int64_t>(P, nsl + 1);
+            launch_k1_count(a, cnt_row, cnt, row_of, slots, s);
+            size_t bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, slots, off, (int)(nsl + 1), s);
+            void* tmp = nullptr;
+            CK(cudaMallocAsync(&tmp, bytes + 16, s));
+            cub::DeviceScan::ExclusiveSum(tmp, bytes, slots, off, (int)(nsl + 1), s);
+            CK(cudaFreeAsync(tmp, s));
+            // longest row: slot 0 of each window holds the window's longest
+            int* d_max = dalloc<int>(P, 1);
+            bytes = 0;
+            cub::DeviceReduce::Max(nullptr, bytes, cnt, d_max, (int)rows, s);
+            CK(cudaMallocAsync(&tmp, bytes + 16, s));
+            cub::DeviceReduce::Max(tmp, bytes, cnt, d_max, (int)rows, s);
+            CK(cudaFreeAsync(tmp, s));
+            int64_t total = 0;
+            int longest = 0;
+            CK(cudaMemcpyAsync(&total, off + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&longest, d_max, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            dfree(P, slots);
+            dfree(P, cnt_row);
+            dfree(P, d_max);
+            size_t free_b = 0, tot_b = 0;
+            CK(cudaMemGetInfo(&free_b, &tot_b));
+            const double need = (double)total * (sizeof(int) + sizeof(double));
+            const bool fits = total < ((int64_t)1 << 31) && need < 0.9 * (double)free_b;
+            const bool want = e ? true : (need <= 0.5 * (double)free_b && longest <= 1024);
+            if (rows > 0 && fits && want) {
+                // small charge vectors stay L2-resident in caller order: K1 then
+                // reads q directly and need not wait for the permutation
+                P->k1_orig = !P->sharded && N <= 262144;
+                const char* eo = getenv("FFTPIM_K1_ORIG");
+                if (eo && !P->sharded) P->k1_orig = std::string(eo) == "1";
+                P->k1_idx = dalloc<int>(P, total);
+                P->k1_wgt = dalloc<double>(P, total);
+                launch_k1_fill(a, row_of, off, P->k1_orig ? P->src_perm : nullptr, P->k1_idx, P->k1_wgt, s);
+                P->k1_cnt = cnt;
+                P->k1_row = row_of;
+                P->k1_off = off;
+                P->k1_slots = total;
+                if (P->k1_scratch) {
+                    dfree(P, P->k1_scratch);
+                    P->k1_scratch = nullptr;
+                }
+            } else {
+                dfree(P, cnt);
+                dfree(P, row_of);
+                dfree(P, off);
+            }
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+
     // ---- far kernel (farzone.py:100-121, pgf.py:450-462)
     {
         std::vector<double> axes;
@@ -982,6 +1052,12 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.far_q = P->q_sorted;
     a.far_n = P->N;
     a.k1_scratch = P->k1_scratch;
+    a.k1_cnt = P->k1_cnt;
+    a.k1_row = P->k1_row;
+    a.k1_off = P->k1_off;
+    a.k1_q = P->k1_orig ? a.q : P->q_sorted;
+    a.k1_idx = P->k1_idx;
+    a.k1_wgt = P->k1_wgt;
     a.kx0 = 0;
     a.knx = P->near_g.n[0];
     a.gx0 = 0;
@@ -1044,11 +1120,13 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
     }
     for (int64_t b = 0; b < batch; ++b) {
         EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
+        // a K1 reading the caller-order charges starts alongside the permutation
+        if (P->k1_orig) CK(cudaEventRecord(P->ev_start, s));
         launch_permute_q(a, s);
         CK(cudaEventRecord(P->ev_fork, s));
         cudaStream_t sn = P->aux[0], sc = P->aux[1], sf = P->aux[2];
         if (parts & FFTPIM_NEAR) {
-            CK(cudaStreamWaitEvent(sn, P->ev_fork, 0));
+            CK(cudaStreamWaitEvent(sn, P->k1_orig ? P->ev_start : P->ev_fork, 0));
             launch_near_project(a, sn);
             if (P->custom_fft) {
                 for (int k = 0; k < 5; ++k)
@@ -1357,6 +1435,7 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
         CK(cudaStreamCreateWithFlags(&P->build_stream, cudaStreamNonBlocking));
         for (auto& st : P->aux) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming));
         for (auto& e : P->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         P->status = dalloc<DevStatus>(P, 1);
         CK(cudaMemsetAsync(P->status, 0, sizeof(DevStatus), P->build_stream));
@@ -1621,6 +1700,7 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
             cudaStreamDestroy(st);
         }
     if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
+    if (plan->ev_start) cudaEventDestroy(plan->ev_start);
     for (auto e : plan->ev_join)
         if (e) cudaEventDestroy(e);
     if (plan->build_stream) cudaStreamDestroy(plan->build_stream);

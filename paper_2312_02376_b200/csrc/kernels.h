@@ -97,6 +97,12 @@ struct EvalArgs {
     int go1, go2;
     int kx0, knx;               // K1 computes planes [kx0, kx0 + knx) (slab shards)
     cplx* k1_scratch;           // tap-major K1 block tiles (null: gather K1)
+    const int* k1_cnt;          // sliced-ELL K1 (null: computed K1): entries per slot
+    const int* k1_row;          // node of each slot
+    const int64_t* k1_off;      // first entry of each 32-slot slice
+    const int* k1_idx;          // source index per entry (into k1_q)
+    const double* k1_wgt;       // weight product per entry
+    const cplx* k1_q;           // charges K1 reads: q_sorted, or q itself (k1_orig)
     const cplx* interp_grid;    // near potentials on the grid, indexed (((x-gx0)*gi1 + y)*gi2 + z)
     int gi1, gi2;
     int gx0;
@@ -130,6 +136,10 @@ struct EvalArgs {
 void launch_permute_q(const EvalArgs& a, cudaStream_t s);
 int64_t k1_scratch_elems(const StencilGeom& g, int knx);
 void launch_near_project(const EvalArgs& a, cudaStream_t s);
+void launch_k1_count(const EvalArgs& a, int* cnt_row, int* cnt_sorted, int* row_of, int64_t* slots,
+                     cudaStream_t s);
+void launch_k1_fill(const EvalArgs& a, const int* row_of, const int64_t* off, const int* remap, int* idx,
+                    double* wgt, cudaStream_t s);
 void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s);
 void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);

@@ -130,6 +130,13 @@ struct FftpimPlan {
     cufftHandle fft_plan = 0;
     cplx* q_sorted = nullptr;     // (N) charges permuted to sorted order
     cplx* k1_scratch = nullptr;   // tap-major K1 extended block tiles
+    int* k1_cnt = nullptr;        // sliced-ELL K1 (eval_kernels.cu): entries per slot
+    int* k1_row = nullptr;        // node of each slot
+    int64_t* k1_off = nullptr;    // (slices + 1) entry offsets
+    bool k1_orig = false;         // entries index the caller-order charges
+    int* k1_idx = nullptr;
+    double* k1_wgt = nullptr;
+    int64_t k1_slots = 0;
 
     // corrections (CSR over sorted observers)
     int64_t* pair_ptr = nullptr;  // (M+1)
@@ -193,6 +200,7 @@ struct FftpimPlan {
     // concurrent evaluation schedule (near chain | K4 | far chain)
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_start = nullptr;
     cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
 
     DevStatus* status = nullptr;
