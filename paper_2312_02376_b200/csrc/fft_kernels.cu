@@ -15,6 +15,8 @@
 // autosort FFT (radix 4, 2, 3, 5 specialised; any other radix <= 32 generic)
 // using a host-computed twiddle table.  Traffic: ~33 n^3 complex values per
 // evaluation instead of ~130 n^3 for full transforms.
+#include <cstdlib>
+
 #include "geom.cuh"
 #include "kernels.h"
 
@@ -316,10 +318,213 @@ static bool launch_fft_stage_p2(const FftStage& st, cudaStream_t s) {
            p2_launch<256>(st, s) || p2_launch<512>(st, s) || p2_launch<1024>(st, s);
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident column FFTs, L = E * T with E = 16 values per thread and
+// T = L / 16 threads per column (L = 64, 128, 256).  Thread t of a column holds
+// x[t + T j] (j < E); the transform is the two-level split
+//   X[k1 + E k2] = sum_t w_T^{t k2} w_L^{t k1} sum_j x[t + T j] w_E^{j k1}
+// -- an E-point DFT in registers, the twiddle, one shared-memory exchange and
+// E/T T-point DFTs in registers, leaving X[(t + T s) + E k2] in a[s T + k2].
+// The inverse runs the same split backwards and returns x[t + T n1] to a[n1],
+// the layout the column was loaded in, so the fused x stage (forward, spectrum
+// multiply, inverse) needs exactly two exchanges and no other shared traffic.
+// Global access: z stages (unit stride along the transform) put a column's T
+// threads on consecutive lanes; x/y stages put consecutive columns (unit
+// stride apart) on consecutive lanes.
+__constant__ double c_cos32[32] = {
+    1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452, 0.7071067811865476, 0.5555702330196023,
+    0.38268343236508984, 0.19509032201612833, 0.0, -0.19509032201612833, -0.38268343236508984, -0.5555702330196023,
+    -0.7071067811865476, -0.8314696123025452, -0.9238795325112867, -0.9807852804032304, -1.0, -0.9807852804032304,
+    -0.9238795325112867, -0.8314696123025452, -0.7071067811865476, -0.5555702330196023, -0.38268343236508984,
+    -0.19509032201612833, -0.0, 0.19509032201612833, 0.38268343236508984, 0.5555702330196023, 0.7071067811865476,
+    0.8314696123025452, 0.9238795325112867, 0.9807852804032304};
+__constant__ double c_sin32[32] = {
+    0.0, 0.19509032201612833, 0.38268343236508984, 0.5555702330196023, 0.7071067811865476, 0.8314696123025452,
+    0.9238795325112867, 0.9807852804032304, 1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452,
+    0.7071067811865476, 0.5555702330196023, 0.38268343236508984, 0.19509032201612833, -0.0, -0.19509032201612833,
+    -0.38268343236508984, -0.5555702330196023, -0.7071067811865476, -0.8314696123025452, -0.9238795325112867,
+    -0.9807852804032304, -1.0, -0.9807852804032304, -0.9238795325112867, -0.8314696123025452, -0.7071067811865476,
+    -0.5555702330196023, -0.38268343236508984, -0.19509032201612833};
+
+// exp(SIGN * 2 pi i e / 32)
+template <int SIGN>
+__device__ __forceinline__ cplx w32(int e) {
+    e &= 31;
+    return cplx{c_cos32[e], SIGN < 0 ? -c_sin32[e] : c_sin32[e]};
+}
+
+// one Stockham pass of radix R (span P) over N register values, x -> y
+template <int N, int R, int P, int SIGN>
+__device__ __forceinline__ void rpass(const cplx (&x)[N], cplx (&y)[N]) {
+    constexpr int M = N / R, S = 32 / (R * P);   // w_{RP}^{qk} = w_32^{qkS}
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const int k = j % P, base = (j / P) * P * R + k;
+        if (R == 4) {
+            cplx a0 = x[j], a1 = x[j + M], a2 = x[j + 2 * M], a3 = x[j + 3 * M];
+            if (k) {
+                a1 = a1 * w32<SIGN>(k * S);
+                a2 = a2 * w32<SIGN>(2 * k * S);
+                a3 = a3 * w32<SIGN>(3 * k * S);
+            }
+            const cplx t0 = a0 + a2, t1 = a0 - a2, t2 = a1 + a3, t3 = mul_si(a1 - a3, SIGN);
+            y[base] = t0 + t2;
+            y[base + P] = t1 + t3;
+            y[base + 2 * P] = t0 - t2;
+            y[base + 3 * P] = t1 - t3;
+        } else {
+            cplx a0 = x[j], a1 = x[j + M];
+            if (k) a1 = a1 * w32<SIGN>(k * S);
+            y[base] = a0 + a1;
+            y[base + P] = a0 - a1;
+        }
+    }
+}
+
+// natural-order N-point DFT (N | 32) of a register array, in place
+template <int N, int SIGN, int P = 1>
+__device__ __forceinline__ void dft_reg(cplx (&a)[N]) {
+    if constexpr (P < N) {
+        constexpr int R = (N / P >= 4) ? 4 : 2;
+        cplx b[N];
+        rpass<N, R, P, SIGN>(a, b);
+#pragma unroll
+        for (int i = 0; i < N; ++i) a[i] = b[i];
+        dft_reg<N, SIGN, P * R>(a);
+    }
+}
+
+// w_L^{SIGN m}, m < L, from the plan's table exp(-2 pi i m / L)
+template <int SIGN>
+__device__ __forceinline__ cplx twl(const cplx* __restrict__ tw, int m) {
+    const double2 w = __ldg(reinterpret_cast<const double2*>(tw) + m);
+    return SIGN < 0 ? cplx{w.x, w.y} : cplx{w.x, -w.y};
+}
+
+template <int L, int SIGN>
+__device__ __forceinline__ void reg_fwd(cplx (&a)[16], cplx* buf, int t, const cplx* tw) {
+    constexpr int E = 16, T = L / E;
+    dft_reg<E, SIGN>(a);
+#pragma unroll
+    for (int k1 = 1; k1 < E; ++k1) a[k1] = a[k1] * twl<SIGN>(tw, (t * k1) & (L - 1));
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) buf[k1 * (T + 1) + t] = a[k1];
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < E / T; ++s) {
+        cplx b[T];
+        const cplx* row = buf + (t + T * s) * (T + 1);
+#pragma unroll
+        for (int u = 0; u < T; ++u) b[u] = row[u];
+        dft_reg<T, SIGN>(b);
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) a[s * T + k2] = b[k2];
+    }
+}
+
+// inverse of the layout reg_fwd leaves (unnormalised, sign +1)
+template <int L>
+__device__ __forceinline__ void reg_inv(cplx (&a)[16], cplx* buf, int t, const cplx* tw) {
+    constexpr int E = 16, T = L / E;
+    __syncthreads();   // buf reuse
+#pragma unroll
+    for (int s = 0; s < E / T; ++s) {
+        const int k1 = t + T * s;
+        cplx b[T];
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) b[k2] = a[s * T + k2];
+        dft_reg<T, +1>(b);
+        cplx* row = buf + k1 * (T + 1);
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) row[n2] = n2 ? b[n2] * twl<+1>(tw, (k1 * n2) & (L - 1)) : b[n2];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) a[k1] = buf[k1 * (T + 1) + t];
+    dft_reg<E, +1>(a);
+}
+
+#define RF_THREADS 128
+template <int L, bool ZC>
+__global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
+    constexpr int E = 16, T = L / E, CPB = RF_THREADS / T, CS = E * (T + 1) + 1;
+    extern __shared__ cplx xs[];
+    const int c = ZC ? threadIdx.x / T : threadIdx.x % CPB;
+    const int t = ZC ? threadIdx.x % T : threadIdx.x / CPB;
+    const int col = blockIdx.x * CPB + c;
+    const bool okc = col < st.nb0;
+    const cplx* __restrict__ in = st.in + (int64_t)blockIdx.y * st.in_s1 + (int64_t)col * st.in_s0;
+    cplx a[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const int i = t + T * j;
+        a[j] = (okc && i < st.lin) ? in[(int64_t)i * st.in_stride] : mk(0.0);
+    }
+    cplx* buf = xs + c * CS;
+    cplx* out = st.out + (int64_t)blockIdx.y * st.out_s1 + (int64_t)col * st.out_s0;
+    if (st.spec) {
+        reg_fwd<L, -1>(a, buf, t, st.tw);
+        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + (int64_t)col * st.spec_s0;
+        if (okc) {
+#pragma unroll
+            for (int s = 0; s < E / T; ++s)
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2)
+                    a[s * T + k2] = a[s * T + k2] * sp[(int64_t)(t + T * s + E * k2) * st.spec_stride];
+        }
+        reg_inv<L>(a, buf, t, st.tw);
+#pragma unroll
+        for (int n1 = 0; n1 < E; ++n1) {
+            const int i = t + T * n1;
+            if (okc && i < st.lout) out[(int64_t)i * st.out_stride] = a[n1];
+        }
+        return;
+    }
+    if (st.sign < 0)
+        reg_fwd<L, -1>(a, buf, t, st.tw);
+    else
+        reg_fwd<L, +1>(a, buf, t, st.tw);
+#pragma unroll
+    for (int s = 0; s < E / T; ++s)
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) {
+            const int k = t + T * s + E * k2;
+            if (okc && k < st.lout) out[(int64_t)k * st.out_stride] = a[s * T + k2];
+        }
+}
+
+template <int L>
+static bool reg_launch(const FftStage& st, cudaStream_t s) {
+    if (st.L != L) return false;
+    constexpr int T = L / 16, CPB = RF_THREADS / T, CS = 16 * (T + 1) + 1;
+    const size_t smem = (size_t)CPB * CS * sizeof(cplx);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_fft_reg<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_reg<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid((st.nb0 + CPB - 1) / CPB, st.nb1);
+    if (st.in_stride == 1)
+        k_fft_reg<L, true><<<grid, RF_THREADS, smem, s>>>(st);
+    else
+        k_fft_reg<L, false><<<grid, RF_THREADS, smem, s>>>(st);
+    return true;
+}
+
+static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
+    static const bool off = [] {
+        const char* e = getenv("FFTPIM_FFT_REG");
+        return e && e[0] == '0';
+    }();
+    if (off) return false;
+    return reg_launch<64>(st, s) || reg_launch<128>(st, s) || reg_launch<256>(st, s);
+}
+
 size_t fft_stage_smem(const FftStage& st) { return (size_t)(2 * st.B * (st.L + 1) + st.L + st.ntwp) * sizeof(cplx); }
 
 void launch_fft_stage(const FftStage& st, cudaStream_t s) {
-    if (launch_fft_stage_p2(st, s)) {
+    if (launch_fft_stage_reg(st, s) || launch_fft_stage_p2(st, s)) {
         fftpim_count_launch();
         return;
     }
