@@ -99,8 +99,8 @@ typedef struct FftpimPlan FftpimPlan;
 FFTPIM_API int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out);
 
 /* u = eval_near + eval_far for `batch` charge vectors.  q: (batch, n_src)
- * complex128 and u: (batch, n_obs) complex128, both DEVICE pointers, stream
- * ordered on `stream` (cudaStream_t; NULL = legacy default).  Replaces
+ * complex128 and u: (batch, n_obs) complex128, both DEVICE pointers aligned
+ * to 16 bytes (FFTPIM_VALUE otherwise), stream ordered on `stream` (cudaStream_t; NULL = legacy default).  Replaces
  * SolvePlan.evaluate (solver.py:24-25); parts selects eval_near / eval_far. */
 FFTPIM_API int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch,
                          int32_t parts, void* stream);

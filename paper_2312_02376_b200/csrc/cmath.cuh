@@ -11,7 +11,7 @@
 
 #define FP_HD __host__ __device__ __forceinline__
 
-struct cplx {
+struct __align__(16) cplx {   // 16-byte aligned: one 128-bit load or store per value
     double re, im;
 };
 

@@ -87,8 +87,10 @@ bool launch_near_project_tiled(const EvalArgs& a, cudaStream_t s);
 // hold K1 as a sliced-ELL matrix over the grid nodes (rows).  Within each window
 // of K1E_WIN consecutive rows the rows are ordered by decreasing length
 // (k1_row), so the 32 rows of a slice have nearly equal lengths; entry k of slot
-// t (= sorted position) lives at off[t / 32] + 32 k + t % 32 (int32 source
-// index, fp64 weight product).  Each row lists its points in the gather K1's
+// t (= sorted position) lives at off[t / 32] + 128 (k / 4) + 4 (t % 32) + k % 4
+// (int32 source index, fp64 weight product): groups of four entries per lane,
+// one 16-byte index load and two 16-byte weight loads per group, the warp's
+// loads contiguous.  Each row lists its points in the gather K1's
 // order (ia, ib, ascending point) with the same weight expression, so the
 // evaluation sums are bit-identical to k_near_project's.
 #define K1E_WIN 256
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(256) k_k1_rows(EvalArgs a, int* cnt, const int
     const int64_t r = FILL ? row_of[t] : t;
     const int z = (int)(r % g.n[2]), y = (int)((r / g.n[2]) % g.n[1]),
               x = (int)(r / ((int64_t)g.n[1] * g.n[2])) + a.kx0;
-    const int64_t base = FILL ? off[t >> 5] + (t & 31) : 0;
+    const int64_t base = FILL ? off[t >> 5] + 4 * (t & 31) : 0;
     int n = 0;
     const int wx = g.w[0], wy = g.w[1], wz = g.w[2];
     const int zlo = max(z - (wz - 1), 0), zhi = min(z, g.nc[2] - 1);
@@ -117,8 +119,9 @@ __global__ void __launch_bounds__(256) k_k1_rows(EvalArgs a, int* cnt, const int
                 for (int p = p0; p < p1; ++p) {
                     const double* w = a.src_w + (int64_t)p * 3 * W;
                     const int ic = z - a.src_start[3 * (int64_t)p + 2];
-                    idx[base + 32 * (int64_t)n] = remap ? remap[p] : p;
-                    wgt[base + 32 * (int64_t)n] = (w[ia] * w[W + ib]) * w[2 * W + ic];
+                    const int64_t e = base + 128 * (int64_t)(n >> 2) + (n & 3);
+                    idx[e] = remap ? remap[p] : p;
+                    wgt[e] = (w[ia] * w[W + ib]) * w[2 * W + ic];
                     ++n;
                 }
             } else {
@@ -145,14 +148,15 @@ __global__ void __launch_bounds__(K1E_WIN) k_k1_window_sort(const int* __restric
     }
 }
 
-// 32 * (longest row of the slice), slice s; entry nslices is 0 (exclusive scan)
+// 32 * (longest row of the slice rounded up to 4), slice s; entry nslices is 0
+// (exclusive scan)
 __global__ void k_k1_slice_slots(const int* __restrict__ cnt, int64_t rows, int64_t nslices, int64_t* slots) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s > nslices) return;
     int m = 0;
     if (s < nslices)
         for (int l = 0; l < 32 && 32 * s + l < rows; ++l) m = max(m, cnt[32 * s + l]);
-    slots[s] = 32 * (int64_t)m;
+    slots[s] = 32 * (int64_t)((m + 3) & ~3);
 }
 
 void launch_k1_count(const EvalArgs& a, int* cnt_row, int* cnt_sorted, int* row_of, int64_t* slots,
@@ -187,38 +191,62 @@ void launch_k1_fill(const EvalArgs& a, const int* row_of, const int64_t* off, co
     fftpim_count_launch();
 }
 
-// one thread per slot (grid node): the row's entries eight at a time, all index
-// and weight loads of a chunk issued before its gathers
-#define K1E_U 8
-__global__ void __launch_bounds__(256) k_k1_spmv(EvalArgs a) {
+// one thread per slot (grid node).  Every lane of a slice runs the slice's
+// longest row rounded up to 4 (windows are sorted by decreasing length, so the
+// slice's first slot holds it); padding entries are (index 0, weight 0) and add
+// exact zeros.  The loads are volatile asm so they issue in program order: all
+// index and weight loads of a two-group chunk, then its eight gathers.
+__device__ __forceinline__ int4 ld_cs_i4(const int* p) {
+    int4 v;
+    asm volatile("ld.global.cs.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_cs_d2(const double* p) {
+    double2 v;
+    asm volatile("ld.global.cs.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_d2(const cplx* p) {
+    double2 v;
+    asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(256, 1) k_k1_spmv(EvalArgs a) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int n1 = a.g.n[1], n2 = a.g.n[2];
     if (t >= (int64_t)a.knx * n1 * n2) return;
-    const int n = a.k1_cnt[t];
+    const int G = (a.k1_cnt[t & ~(int64_t)31] + 3) >> 2;   // groups of four
     const int64_t r = a.k1_row[t];
-    const int64_t base = a.k1_off[t >> 5] + (t & 31);
-    const int* __restrict__ ix = a.k1_idx + base;
-    const double* __restrict__ wt = a.k1_wgt + base;
-    const cplx* __restrict__ q = a.k1_q;
+    const int64_t base = a.k1_off[t >> 5] + 4 * (t & 31);
+    const int* ix = a.k1_idx + base;
+    const double* wt = a.k1_wgt + base;
+    const cplx* q = a.k1_q;
     double ar = 0.0, ai = 0.0;
-    for (int k = 0; k < n; k += K1E_U) {
-        int p[K1E_U];
-        double w[K1E_U];
-#pragma unroll
-        for (int j = 0; j < K1E_U; ++j) {
-            const bool ok = k + j < n;
-            p[j] = ok ? __ldcs(ix + 32 * (int64_t)(k + j)) : 0;
-            w[j] = ok ? __ldcs(wt + 32 * (int64_t)(k + j)) : 0.0;
-        }
-        cplx v[K1E_U];
-#pragma unroll
-        for (int j = 0; j < K1E_U; ++j) v[j] = k + j < n ? q[p[j]] : mk(0.0);
-#pragma unroll
-        for (int j = 0; j < K1E_U; ++j)
-            if (k + j < n) {
-                ar += w[j] * v[j].re;
-                ai += w[j] * v[j].im;
-            }
+    int g = 0;
+    for (; g + 2 <= G; g += 2) {
+        const int4 i0 = ld_cs_i4(ix + 128 * g), i1 = ld_cs_i4(ix + 128 * (g + 1));
+        const double2 w0 = ld_cs_d2(wt + 128 * g), w1 = ld_cs_d2(wt + 128 * g + 2);
+        const double2 w2 = ld_cs_d2(wt + 128 * (g + 1)), w3 = ld_cs_d2(wt + 128 * (g + 1) + 2);
+        const double2 v0 = ld_d2(q + i0.x), v1 = ld_d2(q + i0.y), v2 = ld_d2(q + i0.z), v3 = ld_d2(q + i0.w);
+        const double2 v4 = ld_d2(q + i1.x), v5 = ld_d2(q + i1.y), v6 = ld_d2(q + i1.z), v7 = ld_d2(q + i1.w);
+        ar += w0.x * v0.x; ai += w0.x * v0.y;
+        ar += w0.y * v1.x; ai += w0.y * v1.y;
+        ar += w1.x * v2.x; ai += w1.x * v2.y;
+        ar += w1.y * v3.x; ai += w1.y * v3.y;
+        ar += w2.x * v4.x; ai += w2.x * v4.y;
+        ar += w2.y * v5.x; ai += w2.y * v5.y;
+        ar += w3.x * v6.x; ai += w3.x * v6.y;
+        ar += w3.y * v7.x; ai += w3.y * v7.y;
+    }
+    if (g < G) {
+        const int4 i0 = ld_cs_i4(ix + 128 * g);
+        const double2 w0 = ld_cs_d2(wt + 128 * g), w1 = ld_cs_d2(wt + 128 * g + 2);
+        const double2 v0 = ld_d2(q + i0.x), v1 = ld_d2(q + i0.y), v2 = ld_d2(q + i0.z), v3 = ld_d2(q + i0.w);
+        ar += w0.x * v0.x; ai += w0.x * v0.y;
+        ar += w0.y * v1.x; ai += w0.y * v1.y;
+        ar += w1.x * v2.x; ai += w1.x * v2.y;
+        ar += w1.y * v3.x; ai += w1.y * v3.y;
     }
     const int z = (int)(r % n2), y = (int)((r / n2) % n1), xl = (int)(r / ((int64_t)n1 * n2));
     a.k1_out[((int64_t)xl * a.go1 + y) * a.go2 + z] = cplx{ar, ai};

@@ -896,6 +896,9 @@ void build(FftpimPlan* P) {
                 if (eo && !P->sharded) P->k1_orig = std::string(eo) == "1";
                 P->k1_idx = dalloc<int>(P, total);
                 P->k1_wgt = dalloc<double>(P, total);
+                // padding slots (shorter rows of a slice): index 0, weight 0
+                CK(cudaMemsetAsync(P->k1_idx, 0, sizeof(int) * total, s));
+                CK(cudaMemsetAsync(P->k1_wgt, 0, sizeof(double) * total, s));
                 launch_k1_fill(a, row_of, off, P->k1_orig ? P->src_perm : nullptr, P->k1_idx, P->k1_wgt, s);
                 P->k1_cnt = cnt;
                 P->k1_row = row_of;
@@ -1506,6 +1509,7 @@ int fftpim_group_create(const FftpimProblem* p, int32_t world, int32_t rank, con
 
 int fftpim_group_evaluate(FftpimGroup* g, const double* q, double* u, void* stream) {
     if (!g || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
         group_evaluate(reinterpret_cast<GroupImpl*>(g), q, u, (cudaStream_t)stream);
         return FFTPIM_OK;
@@ -1531,6 +1535,7 @@ void fftpim_group_destroy(FftpimGroup* g) {
 
 int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts, void* stream) {
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
         evaluate(plan, q, u, batch, parts, (cudaStream_t)stream);
         return FFTPIM_OK;
@@ -1548,14 +1553,59 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
         if (batch > plan->h_batch) {
             dfree(plan, plan->h_q);
             dfree(plan, plan->h_u);
+            if (plan->hgraph_exec) cudaGraphExecDestroy(plan->hgraph_exec);
+            plan->hgraph_exec = nullptr;
             plan->h_q = dalloc<double>(plan, 2 * plan->N * batch);
             plan->h_u = dalloc<double>(plan, 2 * plan->M * batch);
             plan->h_batch = batch;
         }
         size_t qb = sizeof(double) * 2 * plan->N * batch, ub = sizeof(double) * 2 * plan->M * batch;
-        CK(cudaMemcpyAsync(plan->h_q, q, qb, cudaMemcpyHostToDevice, s));
-        evaluate(plan, plan->h_q, plan->h_u, batch, parts, s);
-        CK(cudaMemcpyAsync(u, plan->h_u, ub, cudaMemcpyDeviceToHost, s));
+        auto pinned = [](const void* p) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            return at.type == cudaMemoryTypeHost;
+        };
+        FftpimPlan* P = plan;
+        if (P->use_graphs && pinned(q) && pinned(u)) {
+            // pinned caller buffers: one graph holds the upload, the evaluation
+            // schedule and the download (re-captured when the buffers change)
+            if (!(P->hgraph_exec && P->hg_q == q && P->hg_u == u && P->hg_batch == batch && P->hg_parts == parts)) {
+                if (P->hgraph_exec) cudaGraphExecDestroy(P->hgraph_exec);
+                P->hgraph_exec = nullptr;
+                cudaGraph_t graph = nullptr;
+                CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                P->capturing = true;
+                const long long l0 = g_launches.load();
+                try {
+                    CK(cudaMemcpyAsync(P->h_q, q, qb, cudaMemcpyHostToDevice, s));
+                    evaluate_schedule(P, P->h_q, P->h_u, batch, parts, s);
+                    CK(cudaMemcpyAsync(u, P->h_u, ub, cudaMemcpyDeviceToHost, s));
+                    P->hkernels_per_eval = (int)((g_launches.load() - l0) / batch);
+                } catch (...) {
+                    P->capturing = false;
+                    cudaStreamEndCapture(s, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                P->capturing = false;
+                CK(cudaStreamEndCapture(s, &graph));
+                CK(cudaGraphInstantiate(&P->hgraph_exec, graph, 0));
+                CK(cudaGraphDestroy(graph));
+                P->hg_q = q;
+                P->hg_u = u;
+                P->hg_batch = batch;
+                P->hg_parts = parts;
+            }
+            CK(cudaGraphLaunch(P->hgraph_exec, s));
+            fftpim_count_launch(P->hkernels_per_eval * (int)batch);
+        } else {
+            CK(cudaMemcpyAsync(plan->h_q, q, qb, cudaMemcpyHostToDevice, s));
+            evaluate(plan, plan->h_q, plan->h_u, batch, parts, s);
+            CK(cudaMemcpyAsync(u, plan->h_u, ub, cudaMemcpyDeviceToHost, s));
+        }
         CK(cudaStreamSynchronize(s));
         return FFTPIM_OK;
     } catch (const Fail& f) {
@@ -1693,6 +1743,7 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
     if (plan->build_stream) cudaStreamSynchronize(plan->build_stream);
     if (plan->fft_plan) cufftDestroy(plan->fft_plan);
     if (plan->graph_exec) cudaGraphExecDestroy(plan->graph_exec);
+    if (plan->hgraph_exec) cudaGraphExecDestroy(plan->hgraph_exec);
     for (void* p : plan->allocations) cudaFree(p);
     for (auto st : plan->aux)
         if (st) {

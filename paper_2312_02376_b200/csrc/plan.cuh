@@ -182,6 +182,12 @@ struct FftpimPlan {
     double* h_q = nullptr;
     double* h_u = nullptr;
     int64_t h_batch = 0;
+    cudaGraphExec_t hgraph_exec = nullptr;   // upload + evaluation + download, pinned buffers
+    const double* hg_q = nullptr;
+    double* hg_u = nullptr;
+    int64_t hg_batch = 0;
+    int hg_parts = 0;
+    int hkernels_per_eval = 0;
 
     // slab decomposition: shard `rank` of `world` owns near-grid
     // x-planes [X0, X1), the sorted observers/sources whose stencil starts there
