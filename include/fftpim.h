@@ -88,6 +88,9 @@ typedef struct FftpimInfo {
     int64_t device_bytes;       /* plan-owned device memory */
     double build_seconds;
     int32_t real_coefficients;  /* 1: correction coefficients stored as fp64 (NPSP) */
+    int32_t k1_operator;        /* 1: projection held as the plan-time sliced-ELL operator */
+    int32_t custom_fft;         /* 1: pruned column-FFT stages, 0: cuFFT full transforms */
+    int64_t k1_slots;           /* sliced-ELL entries including padding */
 } FftpimInfo;
 
 typedef struct FftpimPlan FftpimPlan;

@@ -42,7 +42,8 @@ class Info(C.Structure):
         ("n_self_pairs", C.c_int64), ("n_wrapped_pairs", C.c_int64),
         ("coincident_kernel_terms", C.c_int64), ("kernel_terms", C.c_int64),
         ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
-        ("real_coefficients", C.c_int32),
+        ("real_coefficients", C.c_int32), ("k1_operator", C.c_int32), ("custom_fft", C.c_int32),
+        ("k1_slots", C.c_int64),
     ]
 
 

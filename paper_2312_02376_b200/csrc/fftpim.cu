@@ -244,7 +244,10 @@ void setup_fft_pipeline(FftpimPlan* P, const int dims[3], cudaStream_t s) {
         if (dims[a] == 1) continue;
         if (L[a] > 2048 || !fft_radices(L[a], rad[a], &nr[a])) return;
     }
+    const char* e = getenv("FFTPIM_FFT");   // "cufft": full cuFFT transforms (unsharded plans)
+    if (e && std::string(e) == "cufft" && !P->sharded) return;
     P->custom_fft = true;
+    P->info.custom_fft = 1;
     for (int a = 0; a < 3; ++a) {
         if (dims[a] == 1) continue;
         std::vector<cplx> tw(L[a]);
@@ -904,6 +907,8 @@ void build(FftpimPlan* P) {
                 P->k1_row = row_of;
                 P->k1_off = off;
                 P->k1_slots = total;
+                P->info.k1_operator = 1;
+                P->info.k1_slots = total;
                 if (P->k1_scratch) {
                     dfree(P, P->k1_scratch);
                     P->k1_scratch = nullptr;

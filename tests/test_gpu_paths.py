@@ -1,0 +1,91 @@
+"""Equivalence of the alternative device paths a plan can select (same inputs,
+same plan geometry):
+
+* K1: the plan-time sliced-ELL operator vs the computed (gather / tiled /
+  tap-major) projections -- the ELL rows keep the gather order and weight
+  expression, so the potentials agree to rounding of the exact-zero padding;
+* K2: the register-resident column FFTs vs the shared-memory Stockham stages
+  vs cuFFT;
+* the host entry with pinned buffers (one graph: upload, evaluation,
+  download) vs pageable buffers vs the device entry;
+* misaligned device buffers are rejected with FFTPIM_VALUE.
+Each variant is selected by the environment variable the library reads at
+plan build / first launch, in a fresh process (tests/_variant_eval.py)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RUNNER = os.path.join(HERE, "_variant_eval.py")
+
+
+def run_variant(case, env_extra, tmp_path, tag):
+    out = tmp_path / f"{case}_{tag}.npy"
+    env = dict(os.environ)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, RUNNER, case, str(out)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    info = json.loads(r.stdout.strip().splitlines()[-1])
+    return np.load(out), info
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d", "p2_planar_npsp", "p1_axis_dyn"])
+def test_k1_ell_matches_computed_projection(case, tmp_path):
+    u_ell, i_ell = run_variant(case, {"FFTPIM_K1": "ell"}, tmp_path, "ell")
+    u_gat, i_gat = run_variant(case, {"FFTPIM_K1": "gather"}, tmp_path, "gather")
+    assert i_ell["k1_ell"] and not i_gat["k1_ell"]
+    assert rel_l2(u_ell, u_gat) <= 1e-14
+    if case in ("c1", "blobs3d"):
+        u_tap, i_tap = run_variant(case, {"FFTPIM_K1": "taps"}, tmp_path, "taps")
+        assert rel_l2(u_ell, u_tap) <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d"])
+def test_register_fft_matches_stockham_and_cufft(case, tmp_path):
+    u_reg, _ = run_variant(case, {}, tmp_path, "reg")
+    u_smem, _ = run_variant(case, {"FFTPIM_FFT_REG": "0"}, tmp_path, "smem")
+    u_cufft, i_cufft = run_variant(case, {"FFTPIM_FFT": "cufft"}, tmp_path, "cufft")
+    assert not i_cufft["custom_fft"]
+    assert rel_l2(u_reg, u_smem) <= 1e-13
+    assert rel_l2(u_reg, u_cufft) <= 1e-13
+
+
+def test_host_entries_and_alignment():
+    import torch
+    import paper_2312_02376_b200 as fp
+    from paper_2312_02376_b200 import _native as nat
+    from paper_2312_02376_b200.workloads import CONFIGS, make_inputs
+    w = CONFIGS[1]
+    pos, q = make_inputs(1)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=w.kshift,
+                               regime=fp.Regime(w.regime))
+    plan = fp.build_plan(cfg, fp.TargetBox(w.D), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos),
+                         fp.SolverParams(**w.params()))
+    nplan = plan.native
+    q = q.astype(np.complex128)
+    u_page = nplan.evaluate(q)
+    q_pin = torch.from_numpy(q).pin_memory()
+    u_pin = torch.empty(q.shape[0], dtype=torch.complex128).pin_memory()
+    for _ in range(3):   # capture, then replays
+        nplan.evaluate(q_pin.numpy(), out=u_pin.numpy())
+    u_dev = nplan.evaluate(torch.from_numpy(q).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(u_pin.numpy(), u_page)
+    np.testing.assert_array_equal(u_dev, u_page)
+    # a new pinned output buffer re-captures the host graph
+    u_pin2 = torch.empty_like(u_pin).pin_memory()
+    nplan.evaluate(q_pin.numpy(), out=u_pin2.numpy())
+    np.testing.assert_array_equal(u_pin2.numpy(), u_page)
+    # misaligned device pointers
+    buf = torch.zeros(2 * q.shape[0] + 2, dtype=torch.float64, device="cuda")
+    good = torch.zeros(2 * q.shape[0], dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        nplan.evaluate_into(buf.data_ptr() + 8, good.data_ptr(), 1, nat.ALL, 0)
