@@ -209,11 +209,14 @@ __device__ __forceinline__ cplx corr_of_row(const EvalArgs& a, int64_t i) {
     return s;
 }
 
-template <int W, int WF>
+// MODE 0: near + far + K4 fix-up -> u.  MODE 1 (off the near chain, once the
+// far chain and K4 are done): far + fix-up -> obs_pre.  MODE 2 (after the
+// inverse FFT): near + obs_pre -> u.
+template <int W, int WF, int MODE>
 __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
     extern __shared__ cplx sfar[];
     const int nfx = a.fo.n[0], nfy = a.fo.n[1], nfz = a.fo.n[2];
-    if (a.parts & FFTPIM_FAR) {
+    if ((a.parts & FFTPIM_FAR) && MODE != 2) {
         for (int t = threadIdx.x; t < nfx * nfy * nfz; t += blockDim.x) sfar[t] = a.far_ug[t];
         __syncthreads();
     }
@@ -223,14 +226,19 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
     const bool active = i < a.M;
     const int64_t ii = active ? i : a.M - 1;
     double ar = 0.0, ai = 0.0;
-    if ((a.parts & FFTPIM_NEAR) && active && sub == OBS_LPO - 1) {
+    if ((a.parts & FFTPIM_NEAR) && MODE != 2 && active && sub == OBS_LPO - 1) {
         // the observer's K4 segments, fetched by the last lane up front so the
         // dependent pointer chain overlaps the interpolation gathers
         const cplx c = corr_of_row(a, i);
         ar = c.re;
         ai = c.im;
     }
-    if (a.parts & FFTPIM_NEAR) {
+    if (MODE == 2 && active && sub == OBS_LPO - 1) {
+        const cplx c = a.obs_pre[i];
+        ar = c.re;
+        ai = c.im;
+    }
+    if ((a.parts & FFTPIM_NEAR) && MODE != 1) {
         // lanes split each stencil row along z (lane sub takes z taps sub, sub+4, ...)
         // so the observer's lanes read one contiguous row per load
         const double* w = a.obs_w + ii * 3 * W;
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
             }
         }
     }
-    if (a.parts & FFTPIM_FAR) {
+    if ((a.parts & FFTPIM_FAR) && MODE != 2) {
         const double* w = a.obs_fw + ii * 3 * WF;
         const int* st = a.obs_fstart + 3 * ii;
         const int s0 = st[0], s1 = st[1], s2 = st[2];
@@ -310,32 +318,52 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
         ar += __shfl_xor_sync(0xffffffffu, ar, o);
         ai += __shfl_xor_sync(0xffffffffu, ai, o);
     }
-    if (active && sub == 0) a.u[a.obs_perm[i]] = cplx{ar, ai};
-}
-
-template <int W>
-static void obs_dispatch_far(const EvalArgs& a, int blocks, size_t smem, cudaStream_t s) {
-    switch (a.fo.order + 1) {
-        case 2: k_observers<W, 2><<<blocks, 256, smem, s>>>(a); break;
-        case 3: k_observers<W, 3><<<blocks, 256, smem, s>>>(a); break;
-        case 4: k_observers<W, 4><<<blocks, 256, smem, s>>>(a); break;
-        case 5: k_observers<W, 5><<<blocks, 256, smem, s>>>(a); break;
-        case 6: k_observers<W, 6><<<blocks, 256, smem, s>>>(a); break;
-        default: k_observers<W, 7><<<blocks, 256, smem, s>>>(a); break;
+    if (active && sub == 0) {
+        if (MODE == 1)
+            a.obs_pre[i] = cplx{ar, ai};
+        else
+            a.u[a.obs_perm[i]] = cplx{ar, ai};
     }
 }
 
-void launch_observers(const EvalArgs& a, cudaStream_t s) {
+template <int W, int MODE>
+static void obs_dispatch_far(const EvalArgs& a, int blocks, size_t smem, cudaStream_t s) {
+    switch (a.fo.order + 1) {
+        case 2: k_observers<W, 2, MODE><<<blocks, 256, smem, s>>>(a); break;
+        case 3: k_observers<W, 3, MODE><<<blocks, 256, smem, s>>>(a); break;
+        case 4: k_observers<W, 4, MODE><<<blocks, 256, smem, s>>>(a); break;
+        case 5: k_observers<W, 5, MODE><<<blocks, 256, smem, s>>>(a); break;
+        case 6: k_observers<W, 6, MODE><<<blocks, 256, smem, s>>>(a); break;
+        default: k_observers<W, 7, MODE><<<blocks, 256, smem, s>>>(a); break;
+    }
+}
+
+// mode 0: the fused pass; 1: far + fix-up into obs_pre; 2: near + obs_pre
+void launch_observers(const EvalArgs& a, cudaStream_t s, int mode) {
     if (a.M == 0) return;
     const int blocks = nblk64(a.M * OBS_LPO, 256);
-    const size_t smem = (a.parts & FFTPIM_FAR) ? (size_t)a.fo.n[0] * a.fo.n[1] * a.fo.n[2] * sizeof(cplx) : 0;
-    switch (a.g.order + 1) {
-        case 2: obs_dispatch_far<2>(a, blocks, smem, s); break;
-        case 3: obs_dispatch_far<3>(a, blocks, smem, s); break;
-        case 4: obs_dispatch_far<4>(a, blocks, smem, s); break;
-        case 5: obs_dispatch_far<5>(a, blocks, smem, s); break;
-        case 6: obs_dispatch_far<6>(a, blocks, smem, s); break;
-        default: obs_dispatch_far<7>(a, blocks, smem, s); break;
+    const size_t smem =
+        ((a.parts & FFTPIM_FAR) && mode != 2) ? (size_t)a.fo.n[0] * a.fo.n[1] * a.fo.n[2] * sizeof(cplx) : 0;
+    if (mode == 1) {
+        obs_dispatch_far<2, 1>(a, blocks, smem, s);
+    } else if (mode == 2) {
+        switch (a.g.order + 1) {
+            case 2: k_observers<2, 2, 2><<<blocks, 256, 0, s>>>(a); break;
+            case 3: k_observers<3, 2, 2><<<blocks, 256, 0, s>>>(a); break;
+            case 4: k_observers<4, 2, 2><<<blocks, 256, 0, s>>>(a); break;
+            case 5: k_observers<5, 2, 2><<<blocks, 256, 0, s>>>(a); break;
+            case 6: k_observers<6, 2, 2><<<blocks, 256, 0, s>>>(a); break;
+            default: k_observers<7, 2, 2><<<blocks, 256, 0, s>>>(a); break;
+        }
+    } else {
+        switch (a.g.order + 1) {
+            case 2: obs_dispatch_far<2, 0>(a, blocks, smem, s); break;
+            case 3: obs_dispatch_far<3, 0>(a, blocks, smem, s); break;
+            case 4: obs_dispatch_far<4, 0>(a, blocks, smem, s); break;
+            case 5: obs_dispatch_far<5, 0>(a, blocks, smem, s); break;
+            case 6: obs_dispatch_far<6, 0>(a, blocks, smem, s); break;
+            default: obs_dispatch_far<7, 0>(a, blocks, smem, s); break;
+        }
     }
     fftpim_count_launch();
 }

@@ -453,6 +453,16 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
     const int t = ZC ? threadIdx.x % T : threadIdx.x / CPB;
     const int col = blockIdx.x * CPB + c;
     const bool okc = col < st.nb0;
+    if (st.spec && st.spec_s0 == 1) {
+        // pull this block's spectrum rows (CPB consecutive columns per k) into L2
+        // now; they are read after the forward transform
+        const int ncols = min(CPB, st.nb0 - (int)blockIdx.x * CPB);
+        const cplx* sp0 = st.spec + (int64_t)blockIdx.y * st.spec_s1 + (int64_t)blockIdx.x * CPB;
+        for (int k = threadIdx.x; k < L; k += RF_THREADS)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sp0 + (int64_t)k * st.spec_stride),
+                         "r"(ncols * (int)sizeof(cplx))
+                         : "memory");
+    }
     const cplx* __restrict__ in = st.in + (int64_t)blockIdx.y * st.in_s1 + (int64_t)col * st.in_s0;
     cplx a[E];
 #pragma unroll

@@ -988,6 +988,8 @@ void build(FftpimPlan* P) {
         P->far_qg = dalloc<cplx>(P, nf);
         P->far_ug = dalloc<cplx>(P, nf);
     }
+    if (npairs <= 500000000LL && getenv("FFTPIM_OBS_FUSED") == nullptr)
+        P->obs_pre = dalloc<cplx>(P, Mown);   // split observer pass (concurrent schedule)
     CK(cudaStreamSynchronize(s));
     dfree(P, d_cnt);
     dfree(P, d_src);
@@ -1133,6 +1135,15 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         launch_permute_q(a, s);
         CK(cudaEventRecord(P->ev_fork, s));
         cudaStream_t sn = P->aux[0], sc = P->aux[1], sf = P->aux[2];
+        // split observer pass: far interpolation + K4 fix-up run off the near
+        // chain; the final pass after the inverse FFT only interpolates the near grid
+        const bool split = parts == FFTPIM_ALL && P->obs_pre != nullptr;
+        if (parts & FFTPIM_FAR) {
+            CK(cudaStreamWaitEvent(sf, P->ev_fork, 0));
+            launch_far_project(a, sf);
+            launch_far_sum(a, sf);
+            CK(cudaEventRecord(P->ev_join[2], sf));
+        }
         if (parts & FFTPIM_NEAR) {
             CK(cudaStreamWaitEvent(sn, P->k1_orig ? P->ev_start : P->ev_fork, 0));
             launch_near_project(a, sn);
@@ -1159,18 +1170,24 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
                 ac.corr_blocks = cb;
                 launch_corr_tiles(ac, sc);
             }
+            if (split) {
+                EvalArgs ap = a;
+                ap.obs_pre = P->obs_pre;
+                CK(cudaStreamWaitEvent(sc, P->ev_join[2], 0));
+                launch_observers(ap, sc, 1);
+            }
             CK(cudaEventRecord(P->ev_join[1], sc));
             CK(cudaStreamWaitEvent(s, P->ev_join[0], 0));
             CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));
         }
-        if (parts & FFTPIM_FAR) {
-            CK(cudaStreamWaitEvent(sf, P->ev_fork, 0));
-            launch_far_project(a, sf);
-            launch_far_sum(a, sf);
-            CK(cudaEventRecord(P->ev_join[2], sf));
-            CK(cudaStreamWaitEvent(s, P->ev_join[2], 0));
+        if (parts & FFTPIM_FAR) CK(cudaStreamWaitEvent(s, P->ev_join[2], 0));
+        if (split) {
+            EvalArgs ap = a;
+            ap.obs_pre = P->obs_pre;
+            launch_observers(ap, s, 2);
+        } else {
+            launch_observers(a, s);
         }
-        launch_observers(a, s);
     }
     CK(cudaGetLastError());
 }

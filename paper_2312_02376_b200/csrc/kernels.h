@@ -131,6 +131,7 @@ struct EvalArgs {
     int far_blocks, far_warps;
     const cplx* far_q;          // sources projected onto the far grid (own range for shards)
     int64_t far_n;
+    cplx* obs_pre;              // far + K4 fix-up per sorted observer (split observer pass)
     int parts;
 };
 void launch_permute_q(const EvalArgs& a, cudaStream_t s);
@@ -145,7 +146,7 @@ void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);
 void launch_axpy(cplx* acc, const cplx* x, int64_t n, cudaStream_t s);   // acc += x
-void launch_observers(const EvalArgs& a, cudaStream_t s);
+void launch_observers(const EvalArgs& a, cudaStream_t s, int mode = 0);   // 0 fused, 1 pre, 2 post
 
 // ---- pruned column-FFT stages (fft_kernels.cu)
 size_t fft_stage_smem(const FftStage& st);

@@ -166,6 +166,7 @@ struct FftpimPlan {
     cplx* far_qg = nullptr;       // projected far source grid
     cplx* far_partial = nullptr;  // per-block partial grids
     cplx* far_ug = nullptr;       // far observer-grid potentials
+    cplx* obs_pre = nullptr;      // split observer pass: far + K4 fix-up (concurrent schedule)
     int far_blocks = 0;
     int far_warps = 0;
 
