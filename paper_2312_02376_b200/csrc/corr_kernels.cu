@@ -175,8 +175,9 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.n_pairs == 0) return;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
     // a.corr_blocks caps the grid (the concurrent schedule leaves SMs to the near chain)
-    int cap = 148 * CORR_MINB;
-    if (a.corr_blocks > 0) cap = std::min(cap, a.corr_blocks);
+    int64_t cap = 148 * CORR_MINB;
+    if (a.corr_blocks > 0) cap = std::min<int64_t>(cap, a.corr_blocks);
+    if (a.corr_blocks < 0) cap = INT32_MAX;   // one block per CORR_WARPS tiles (no grid-stride loop)
     const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, cap);
     if (a.coef_r)
         k_corr_tiles<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
@@ -186,9 +187,9 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------- K3 + K5c + fix-up
-// OBS_LPO lanes per observer; every lane walks all W*W stencil rows (ia, ib) and
-// takes the z taps sub, sub + OBS_LPO, ... of each, so one warp load reads one
-// contiguous row per observer.  The far observer grid (<= 48 KB) is staged in
+// OBS_LPO lanes per observer; lane sub takes the entries sub, sub + OBS_LPO, ...
+// of the flattened (y, z) stencil plane for every x row, so a warp load reads
+// each observer's consecutive z taps.  The far observer grid (<= 48 KB) is staged in
 // shared memory.  The last lane fetches the observer's K4 segments, the lanes
 // are reduced with a fixed xor tree and lane 0 stores.  Single-plane axes:
 // weights past the first tap are zero and the indices are clamped, so those
@@ -239,42 +240,35 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
         ai = c.im;
     }
     if ((a.parts & FFTPIM_NEAR) && MODE != 1) {
-        // lanes split each stencil row along z (lane sub takes z taps sub, sub+4, ...)
-        // so the observer's lanes read one contiguous row per load
+        // lane sub takes the entries e = sub, sub + OBS_LPO, ... of the W x W
+        // (y, z) stencil plane, for every x row, so one warp load reads each
+        // observer's consecutive z taps and no lane idles on a partial row
         const double* w = a.obs_w + ii * 3 * W;
         const int* st = a.obs_start + 3 * ii;
         const int c1 = a.gi1, c2 = a.gi2;
         const int m0 = a.g.n[0] - 1, m1 = a.g.n[1] - 1, m2 = a.g.n[2] - 1;
         const int s0 = st[0], s1 = st[1], s2 = st[2];
-        double wx[W], wy[W];
+        constexpr int ET = (W * W + OBS_LPO - 1) / OBS_LPO;
+        double wyz[ET];
+        int off[ET];
 #pragma unroll
-        for (int c = 0; c < W; ++c) {
-            wx[c] = w[c];
-            wy[c] = w[W + c];
-        }
-        constexpr int ZT = (W + OBS_LPO - 1) / OBS_LPO;
-        double wz[ZT];
-        int oz[ZT];
-#pragma unroll
-        for (int t = 0; t < ZT; ++t) {
-            const int ic = sub + t * OBS_LPO;
-            wz[t] = ic < W ? w[2 * W + ic] : 0.0;
-            oz[t] = min(s2 + min(ic, W - 1), m2);
+        for (int t = 0; t < ET; ++t) {
+            const int e = sub + OBS_LPO * t;
+            const bool ok = e < W * W;
+            const int ib = ok ? e / W : 0, ic = ok ? e % W : 0;
+            wyz[t] = ok ? w[W + ib] * w[2 * W + ic] : 0.0;
+            off[t] = min(s1 + ib, m1) * c2 + min(s2 + ic, m2);
         }
 #pragma unroll
         for (int ia = 0; ia < W; ++ia) {
+            const double wxa = w[ia];
             const cplx* plane = a.interp_grid + (int64_t)(min(s0 + ia, m0) - a.gx0) * c1 * c2;
 #pragma unroll
-            for (int ib = 0; ib < W; ++ib) {
-                const double wxy = wx[ia] * wy[ib];
-                const cplx* row = plane + (int64_t)min(s1 + ib, m1) * c2;
-#pragma unroll
-                for (int t = 0; t < ZT; ++t) {
-                    const cplx v = row[oz[t]];
-                    const double wgt = wxy * wz[t];
-                    ar += wgt * v.re;
-                    ai += wgt * v.im;
-                }
+            for (int t = 0; t < ET; ++t) {
+                const cplx v = plane[off[t]];
+                const double wgt = wxa * wyz[t];
+                ar += wgt * v.re;
+                ai += wgt * v.im;
             }
         }
     }
@@ -282,34 +276,27 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
         const double* w = a.obs_fw + ii * 3 * WF;
         const int* st = a.obs_fstart + 3 * ii;
         const int s0 = st[0], s1 = st[1], s2 = st[2];
-        double wx[WF], wy[WF];
+        constexpr int ET = (WF * WF + OBS_LPO - 1) / OBS_LPO;
+        double wyz[ET];
+        int off[ET];
 #pragma unroll
-        for (int c = 0; c < WF; ++c) {
-            wx[c] = w[c];
-            wy[c] = w[WF + c];
-        }
-        constexpr int ZT = (WF + OBS_LPO - 1) / OBS_LPO;
-        double wz[ZT];
-        int oz[ZT];
-#pragma unroll
-        for (int t = 0; t < ZT; ++t) {
-            const int ic = sub + t * OBS_LPO;
-            wz[t] = ic < WF ? w[2 * WF + ic] : 0.0;
-            oz[t] = min(s2 + min(ic, WF - 1), nfz - 1);
+        for (int t = 0; t < ET; ++t) {
+            const int e = sub + OBS_LPO * t;
+            const bool ok = e < WF * WF;
+            const int ib = ok ? e / WF : 0, ic = ok ? e % WF : 0;
+            wyz[t] = ok ? w[WF + ib] * w[2 * WF + ic] : 0.0;
+            off[t] = min(s1 + ib, nfy - 1) * nfz + min(s2 + ic, nfz - 1);
         }
 #pragma unroll
         for (int ia = 0; ia < WF; ++ia) {
+            const double wxa = w[ia];
+            const cplx* plane = sfar + min(s0 + ia, nfx - 1) * nfy * nfz;
 #pragma unroll
-            for (int ib = 0; ib < WF; ++ib) {
-                const double wxy = wx[ia] * wy[ib];
-                const cplx* row = sfar + (min(s0 + ia, nfx - 1) * nfy + min(s1 + ib, nfy - 1)) * nfz;
-#pragma unroll
-                for (int t = 0; t < ZT; ++t) {
-                    const cplx v = row[oz[t]];
-                    const double wgt = wxy * wz[t];
-                    ar += wgt * v.re;
-                    ai += wgt * v.im;
-                }
+            for (int t = 0; t < ET; ++t) {
+                const cplx v = plane[off[t]];
+                const double wgt = wxa * wyz[t];
+                ar += wgt * v.re;
+                ai += wgt * v.im;
             }
         }
     }

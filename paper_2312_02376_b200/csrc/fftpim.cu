@@ -1458,7 +1458,18 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
         memset(&P->info, 0, sizeof(P->info));
         CK(cudaSetDevice(P->device));
         CK(cudaStreamCreateWithFlags(&P->build_stream, cudaStreamNonBlocking));
-        for (auto& st : P->aux) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        {
+            // near chain (aux[0]) at the highest priority: the block scheduler then
+            // serves its latency-bound kernels before the K4 stream (aux[1])
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            static const int prio = [] {
+                const char* e = getenv("FFTPIM_STREAM_PRIO");
+                return e ? atoi(e) : 1;
+            }();
+            const int pr[3] = {prio ? hi : 0, prio ? lo : 0, prio ? (lo + hi) / 2 : 0};
+            for (int k = 0; k < 3; ++k) CK(cudaStreamCreateWithPriority(&P->aux[k], cudaStreamNonBlocking, pr[k]));
+        }
         CK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming));
         for (auto& e : P->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
