@@ -1147,9 +1147,16 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         if (parts & FFTPIM_NEAR) {
             CK(cudaStreamWaitEvent(sn, P->k1_orig ? P->ev_start : P->ev_fork, 0));
             launch_near_project(a, sn);
+            static const int k4_gate = [] {   // 1: K4 starts after K1, 2: after the forward FFT stages
+                const char* e = getenv("FFTPIM_K4_GATE");
+                return e ? atoi(e) : 0;
+            }();
+            if (k4_gate == 1) CK(cudaEventRecord(P->ev_k1, sn));
             if (P->custom_fft) {
-                for (int k = 0; k < 5; ++k)
+                for (int k = 0; k < 5; ++k) {
                     if (P->stage_on[k]) launch_fft_stage(P->stage[k], sn);
+                    if (k == 1 && k4_gate == 2) CK(cudaEventRecord(P->ev_k1, sn));
+                }
             } else {
                 CKFFT(cufftSetStream(P->fft_plan, sn));
                 CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
@@ -1159,6 +1166,7 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
             }
             CK(cudaEventRecord(P->ev_join[0], sn));
             CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
+            if (k4_gate && P->custom_fft) CK(cudaStreamWaitEvent(sc, P->ev_k1, 0));
             {
                 // K4 streams HBM on part of the chip while the latency-bound
                 // near chain runs on the rest (FFTPIM_CORR_BLOCKS tunes the split)
@@ -1196,9 +1204,17 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
               cudaEvent_t* ev = nullptr) {
     if (parts & ~FFTPIM_ALL || parts == 0) throw Fail{FFTPIM_VALUE, "parts must be a non-empty subset of NEAR|FAR"};
     CK(cudaSetDevice(P->device));
-    if (!ev && s != nullptr && P->use_graphs) {
+    if (!ev && P->use_graphs) {
         // replay a captured CUDA graph of the whole evaluation (launch-bound at small N);
-        // re-captured whenever the caller's buffers or the batch change
+        // re-captured whenever the caller's buffers or the batch change.  The
+        // legacy default stream cannot be captured: the graph then runs on a
+        // plan-owned stream fenced by events on both sides.
+        const cudaStream_t caller = s;
+        if (caller == nullptr) {
+            CK(cudaEventRecord(P->ev_in, caller));
+            CK(cudaStreamWaitEvent(P->gstream, P->ev_in, 0));
+            s = P->gstream;
+        }
         if (!(P->graph_exec && P->g_q == q && P->g_u == u && P->g_batch == batch && P->g_parts == parts)) {
             if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);
             P->graph_exec = nullptr;
@@ -1225,6 +1241,10 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
             P->g_parts = parts;
         }
         CK(cudaGraphLaunch(P->graph_exec, s));
+        if (caller == nullptr) {
+            CK(cudaEventRecord(P->ev_out, s));
+            CK(cudaStreamWaitEvent(caller, P->ev_out, 0));
+        }
         fftpim_count_launch(P->kernels_per_eval * (int)batch);
         CK(cudaGetLastError());
         return;
@@ -1472,6 +1492,10 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
         }
         CK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_k1, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_out, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
         for (auto& e : P->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         P->status = dalloc<DevStatus>(P, 1);
         CK(cudaMemsetAsync(P->status, 0, sizeof(DevStatus), P->build_stream));
@@ -1785,6 +1809,10 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
         }
     if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
     if (plan->ev_start) cudaEventDestroy(plan->ev_start);
+    if (plan->ev_in) cudaEventDestroy(plan->ev_in);
+    if (plan->ev_k1) cudaEventDestroy(plan->ev_k1);
+    if (plan->ev_out) cudaEventDestroy(plan->ev_out);
+    if (plan->gstream) cudaStreamDestroy(plan->gstream);
     for (auto e : plan->ev_join)
         if (e) cudaEventDestroy(e);
     if (plan->build_stream) cudaStreamDestroy(plan->build_stream);

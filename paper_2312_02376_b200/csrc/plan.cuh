@@ -208,6 +208,9 @@ struct FftpimPlan {
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr;
     cudaEvent_t ev_start = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaEvent_t ev_k1 = nullptr;                     // K4 gate (FFTPIM_K4_GATE)   // legacy-stream fence around graph replays
+    cudaStream_t gstream = nullptr;                  // graph replay stream for legacy-stream callers
     cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
 
     DevStatus* status = nullptr;
