@@ -212,7 +212,10 @@ __device__ __forceinline__ double2 ld_d2(const cplx* p) {
     return v;
 }
 
-__global__ void __launch_bounds__(256, 1) k_k1_spmv(EvalArgs a) {
+#ifndef K1E_THREADS
+#define K1E_THREADS 256
+#endif
+__global__ void __launch_bounds__(K1E_THREADS, 1) k_k1_spmv(EvalArgs a) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int n1 = a.g.n[1], n2 = a.g.n[2];
     if (t >= (int64_t)a.knx * n1 * n2) return;
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(256, 1) k_k1_spmv(EvalArgs a) {
 
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {
     if (a.k1_off) {
-        k_k1_spmv<<<nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], 256), 256, 0, s>>>(a);
+        k_k1_spmv<<<nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], K1E_THREADS), K1E_THREADS, 0, s>>>(a);
         fftpim_count_launch();
         return;
     }
