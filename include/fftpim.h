@@ -108,6 +108,23 @@ FFTPIM_API int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out);
 FFTPIM_API int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch,
                          int32_t parts, void* stream);
 
+/* Batched excitation sweep (C5).  E <= 64 excitations of one
+ * geometry whose Floquet shifts differ only along the periodic axis `axis`:
+ * excitation e uses p->kshift with component `axis` replaced by
+ * kshift_axis[2e] + i kshift_axis[2e+1].  The plan stores the correction pairs
+ * once with 2 i_d + 1 phase components (nearzone.py:405-457 is linear in the
+ * image phases, pgf.py:114-123), plus kernel_hat and the far kernel per
+ * excitation.  Equivalent to E plans built with fftpim_plan_create. */
+FFTPIM_API int fftpim_sweep_create(const FftpimProblem* p, int32_t axis, int32_t n_exc, const double* kshift_axis,
+                                   FftpimPlan** out);
+
+/* u[e] = evaluate_e(q[e]) for all excitations: q (E, n_src) and u (E, n_obs)
+ * complex128 DEVICE pointers (16-byte aligned), stream ordered. */
+FFTPIM_API int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* stream);
+
+/* axis and excitation count of a sweep plan (-1, 0 for ordinary plans). */
+FFTPIM_API int fftpim_sweep_info(const FftpimPlan* plan, int32_t* axis, int32_t* n_exc);
+
 /* Same with HOST q/u (pinned or pageable): H2D copy, evaluate, D2H copy,
  * synchronous.  This is the call the reference's FFI binding makes. */
 FFTPIM_API int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch,

@@ -11,6 +11,7 @@ from .api import (FarZonePlan, NativePlan, NearZonePlan, SolvePlan, SolveResult,
                   save_far_kernel, solve)
 from .exceptions import (DomainError, KernelCacheError, NativeLibraryError, NotConvergedError,
                          PerisumError, SeparationError, ValidationError, WoodAnomalyError)
+from .sweep import SweepPlan, build_sweep_plan
 from .problem import (ObserverPointSet, Periodicity, PeriodicityConfig, PotentialField, Regime,
                       SolverParams, SourcePointSet, TargetBox, ValidationReport, auto_near_dims,
                       validate_problem)
@@ -24,5 +25,5 @@ __all__ = [
     "NotConvergedError", "PerisumError", "SeparationError", "ValidationError", "WoodAnomalyError",
     "ObserverPointSet", "Periodicity", "PeriodicityConfig", "PotentialField", "Regime",
     "SolverParams", "SourcePointSet", "TargetBox", "ValidationReport", "auto_near_dims",
-    "validate_problem",
+    "validate_problem", "SweepPlan", "build_sweep_plan",
 ]

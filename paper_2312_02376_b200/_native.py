@@ -51,7 +51,7 @@ EXPORTED = ("fftpim_plan_create", "fftpim_plan_evaluate", "fftpim_plan_evaluate_
             "fftpim_plan_info", "fftpim_plan_export", "fftpim_plan_set_far_kernel",
             "fftpim_plan_destroy", "fftpim_last_error", "fftpim_launch_count", "fftpim_plan_profile",
             "fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
-            "fftpim_group_destroy")
+            "fftpim_group_destroy", "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info")
 N_STAGES = 9
 STAGES = ("permute_q", "far_project", "far_sum", "near_project", "fft_forward", "spectrum_mul",
           "fft_inverse", "corr_matvec", "observers")
@@ -89,7 +89,11 @@ def load(path: str = LIB_PATH):
     lib.fftpim_group_info.argtypes = [vp, C.c_int32, C.POINTER(Info)]
     lib.fftpim_group_destroy.argtypes = [vp]
     lib.fftpim_group_destroy.restype = None
-    for name in ("fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info"):
+    lib.fftpim_sweep_create.argtypes = [C.POINTER(Problem), C.c_int32, C.c_int32, vp, C.POINTER(vp)]
+    lib.fftpim_sweep_evaluate.argtypes = [vp, vp, vp, vp]
+    lib.fftpim_sweep_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    for name in ("fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
+                 "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info"):
         getattr(lib, name).restype = C.c_int
     lib.fftpim_last_error.restype = C.c_char_p
     lib.fftpim_launch_count.restype = C.c_int64

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
     if ((a.parts & FFTPIM_NEAR) && MODE != 2 && active && sub == OBS_LPO - 1) {
         // the observer's K4 segments, fetched by the last lane up front so the
         // dependent pointer chain overlaps the interpolation gathers
-        const cplx c = corr_of_row(a, i);
+        const cplx c = a.sw_corr ? a.sw_corr[i * a.sw_E + a.sw_e] : corr_of_row(a, i);
         ar = c.re;
         ai = c.im;
     }

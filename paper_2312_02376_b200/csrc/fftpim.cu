@@ -386,6 +386,116 @@ void setup_fft_pipeline_shard(FftpimPlan* P, const int dims[3], cudaStream_t s) 
 
 EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts);
 
+// Images of G_near for the shift ks (pgf.py:114-123): offsets i*L and phases
+// exp(-j i.(ks o L)), i in [-i_d, i_d]^dim.  axis >= 0 keeps only the images with
+// i[axis] == only and leaves the axis part out of the phase (sweep components).
+static void make_images(const FftpimProblem& pr, const double ks[3][2], ImageSet& im, int axis = -1, int only = 0) {
+    int hw[3];
+    for (int a = 0; a < 3; ++a) hw[a] = a < pr.dim ? pr.i_d : 0;
+    int c = 0;
+    std::complex<double> kl[3];
+    for (int a = 0; a < 3; ++a) kl[a] = std::complex<double>(ks[a][0], ks[a][1]) * pr.L[a];
+    for (int i = -hw[0]; i <= hw[0]; ++i)
+        for (int j = -hw[1]; j <= hw[1]; ++j)
+            for (int k = -hw[2]; k <= hw[2]; ++k) {
+                const int ii[3] = {i, j, k};
+                if (axis >= 0 && ii[axis] != only) continue;
+                double idx[3] = {(double)i, (double)j, (double)k};
+                std::complex<double> dotp(0.0, 0.0);
+                for (int a = 0; a < 3; ++a)
+                    if (a != axis) dotp += idx[a] * kl[a];
+                std::complex<double> ph = std::exp(std::complex<double>(0.0, -1.0) * dotp);
+                for (int a = 0; a < 3; ++a) im.off[c][a] = idx[a] * pr.L[a];
+                im.ph_re[c] = ph.real();
+                im.ph_im[c] = ph.imag();
+                ++c;
+            }
+    im.count = c;
+}
+
+// phase of image code c, exp(-j c.(ks o L)) (nearzone.py:456-457); the sweep
+// axis part left out when axis >= 0
+static void code_phases(const FftpimProblem& pr, const double ks[3][2], PairGeom& pg, int axis = -1) {
+    for (int c = 0; c < pg.ncodes; ++c) {
+        std::complex<double> dotp(0.0, 0.0);
+        for (int a = 0; a < 3; ++a)
+            if (a != axis) dotp += (double)pg.code[c][a] * (std::complex<double>(ks[a][0], ks[a][1]) * pr.L[a]);
+        std::complex<double> ph = std::exp(std::complex<double>(0.0, -1.0) * dotp);
+        pg.phase_re[c] = ph.real();
+        pg.phase_im[c] = ph.imag();
+    }
+}
+
+// kernel_hat = fftn(embed(G_near)) / M for the image set im (nearzone.py:215-235)
+static void tabulate_khat(FftpimPlan* P, const int dims[3], const double h[3], const ImageSet& im, cplx* out,
+                          cudaStream_t s) {
+    launch_embed_table(out, P->cdims, dims, h, im, s);
+    CKFFT(cufftSetStream(P->fft_plan, s));
+    CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)out, (cufftDoubleComplex*)out, CUFFT_FORWARD));
+    fftpim_count_launch(1);
+    launch_scale(out, P->n_fft, 1.0 / (double)P->n_fft, s);   // numpy ifftn's 1/M
+}
+
+// far kernel G_total - G_near on the difference points (farzone.py:100-121,
+// pgf.py:450-462) for the shift ks; returns the worst series length
+static int64_t tabulate_far(FftpimPlan* P, const double ks[3][2], const ImageSet& im, cplx* out, cudaStream_t s) {
+    const FftpimProblem& pr = P->prob;
+    int fdims[3];
+    double fh[3];
+    for (int a = 0; a < 3; ++a) {
+        fdims[a] = P->far_sg.n[a];
+        fh[a] = P->far_sg.h[a];
+    }
+    double maxLp = 0.0;
+    for (int a = 0; a < pr.dim; ++a) maxLp = std::max(maxLp, pr.L[a]);
+    std::vector<double> axes;
+    double zmin = 1e300, zmax = -1e300;
+    for (int a = 0; a < 3; ++a) {
+        int n = fdims[a];
+        double shift = P->far_og.origin[a] - P->far_sg.origin[a];
+        if (n == 1) {
+            axes.push_back(shift);
+            if (a == 2) zmin = zmax = shift;
+        } else {
+            for (int l = -(n - 1); l < n; ++l) {
+                double v = (double)l * fh[a] + shift;
+                axes.push_back(v);
+                if (a == 2) {
+                    zmin = std::min(zmin, v);
+                    zmax = std::max(zmax, v);
+                }
+            }
+        }
+    }
+    double* d_axes = dalloc<double>(P, (int64_t)axes.size());
+    CK(cudaMemcpyAsync(d_axes, axes.data(), sizeof(double) * axes.size(), cudaMemcpyHostToDevice, s));
+    FarSeriesParams fp{};
+    fp.dim = pr.dim;
+    fp.npsp = P->npsp;
+    for (int a = 0; a < 3; ++a) {
+        fp.L[a] = pr.L[a];
+        fp.ks_re[a] = ks[a][0];
+        fp.ks_im[a] = ks[a][1];
+    }
+    fp.k0_re = pr.k0[0];
+    fp.k0_im = pr.k0[1];
+    fp.tol = pr.series_tol;
+    fp.cutoff = std::log(1.0 / pr.series_tol) + 8.0;
+    fp.sep = im.sep_tol;
+    fp.wood = 1e-8 * 2.0 * M_PI / maxLp;
+    fp.zmin = zmin;
+    fp.zmax = zmax;
+    fp.max_terms = 1000000;
+    fp.max_layers = 200000;
+    static const GLTable gl = gauss_laguerre_half();
+    launch_far_series(d_axes, P->far_kdims, fp, im, gl, out, P->status, s);
+    check_status(P, "far kernel tabulation");
+    DevStatus st;
+    CK(cudaMemcpy(&st, P->status, sizeof(st), cudaMemcpyDeviceToHost));
+    dfree(P, d_axes);
+    return st.kernel_terms;
+}
+
 void build(FftpimPlan* P) {
     const FftpimProblem& pr = P->prob;
     cudaStream_t s = P->build_stream;
@@ -472,25 +582,7 @@ void build(FftpimPlan* P) {
     for (int a = 0; a < pr.dim; ++a) maxLp = std::max(maxLp, pr.L[a]);
     im.sing_tol = 1e-12 * std::max(std::max(maxL, maxD), 1.0);   // nearzone.py:213
     im.sep_tol = 1e-13 * std::max(maxLp, 1.0);                     // pgf.py:93-94
-    {
-        int hw[3];
-        for (int a = 0; a < 3; ++a) hw[a] = a < pr.dim ? pr.i_d : 0;
-        int c = 0;
-        std::complex<double> kl[3];
-        for (int a = 0; a < 3; ++a) kl[a] = std::complex<double>(pr.kshift[a][0], pr.kshift[a][1]) * pr.L[a];
-        for (int i = -hw[0]; i <= hw[0]; ++i)
-            for (int j = -hw[1]; j <= hw[1]; ++j)
-                for (int k = -hw[2]; k <= hw[2]; ++k) {
-                    double idx[3] = {(double)i, (double)j, (double)k};
-                    std::complex<double> dotp = idx[0] * kl[0] + idx[1] * kl[1] + idx[2] * kl[2];
-                    std::complex<double> ph = std::exp(std::complex<double>(0.0, -1.0) * dotp);
-                    for (int a = 0; a < 3; ++a) im.off[c][a] = idx[a] * pr.L[a];
-                    im.ph_re[c] = ph.real();
-                    im.ph_im[c] = ph.imag();
-                    ++c;
-                }
-        im.count = c;
-    }
+    make_images(pr, pr.kshift, im);
 
     // ---- points
     double* d_src = dalloc<double>(P, 3 * N);
@@ -563,7 +655,6 @@ void build(FftpimPlan* P) {
 
     // ---- near kernel table -> kernel_hat (nearzone.py:215-235)
     P->khat = dalloc<cplx>(P, P->n_fft);
-    launch_embed_table(P->khat, P->cdims, dims, h, im, s);
     unsigned long long* d_cnt = dalloc<unsigned long long>(P, 4);
     CK(cudaMemsetAsync(d_cnt, 0, 4 * sizeof(unsigned long long), s));
     launch_count_coincident(dims, h, im, d_cnt, s);
@@ -573,10 +664,7 @@ void build(FftpimPlan* P) {
             if (P->cdims[a] > 1) n[rank++] = P->cdims[a];
         if (rank == 0) throw Fail{FFTPIM_VALUE, "near grid has no active axis"};
         CKFFT(cufftPlanMany(&P->fft_plan, rank, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 1));
-        CKFFT(cufftSetStream(P->fft_plan, s));
-        CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->khat, (cufftDoubleComplex*)P->khat, CUFFT_FORWARD));
-        fftpim_count_launch(1);
-        launch_scale(P->khat, P->n_fft, 1.0 / (double)P->n_fft, s);   // numpy ifftn's 1/M
+        tabulate_khat(P, dims, h, im, P->khat, s);
     }
     setup_fft_pipeline(P, dims, s);
     if (P->sharded) setup_fft_pipeline_shard(P, dims, s);
@@ -638,15 +726,7 @@ void build(FftpimPlan* P) {
             pg.code[c][0] = cx;
             pg.code[c][1] = cy;
             pg.code[c][2] = cz;
-            std::complex<double> dotp(0.0, 0.0);
-            for (int a = 0; a < 3; ++a) {
-                double cv = (double)pg.code[c][a];
-                pg.shift[c][a] = cv * pr.L[a];
-                dotp += cv * (std::complex<double>(pr.kshift[a][0], pr.kshift[a][1]) * pr.L[a]);
-            }
-            std::complex<double> ph = std::exp(std::complex<double>(0.0, -1.0) * dotp);
-            pg.phase_re[c] = ph.real();
-            pg.phase_im[c] = ph.imag();
+            for (int a = 0; a < 3; ++a) pg.shift[c][a] = (double)pg.code[c][a] * pr.L[a];
             ++c;
         };
         set_code(0, 0, 0);
@@ -661,6 +741,7 @@ void build(FftpimPlan* P) {
                 for (int cz = rng[2][0]; cz <= rng[2][1]; ++cz)
                     if (cx || cy || cz) set_code(cx, cy, cz);
         pg.ncodes = c;
+        code_phases(pr, pr.kshift, pg);
     }
     // augmented source list: originals, then wrapped copies code by code
     std::vector<int64_t> code_off(pg.ncodes + 1, 0);
@@ -812,34 +893,56 @@ void build(FftpimPlan* P) {
         tab_total += sz;
     }
     cplx* tables = dalloc<cplx>(P, tab_total);
-    launch_code_tables(tb, pg.ncodes, pg, im, tables, tab_total, s);
     // fill pass
     P->pair_src = dalloc<int>(P, npairs);
     // image codes are only needed for operand export; skipped for huge pair counts (C3/C4)
-    if (npairs <= (int64_t)1 << 31) P->pair_codeid = dalloc<unsigned char>(P, npairs);
-    if (P->npsp)
-        P->pair_coef_r = dalloc<double>(P, npairs);
-    else
-        P->pair_coef = dalloc<cplx>(P, npairs);
-    P->info.real_coefficients = P->npsp ? 1 : 0;
+    if (npairs <= (int64_t)1 << 31 || P->sweep) P->pair_codeid = dalloc<unsigned char>(P, npairs);
     pa.pair_ptr = P->pair_ptr;
     pa.tables = tables;
     pa.pair_src = P->pair_src;
     pa.pair_codeid = P->pair_codeid;
-    pa.coef = P->pair_coef;
-    pa.coef_r = P->pair_coef_r;
-    launch_pairs_fill(pg, im, tb, pa, s);
+    if (P->sweep) {
+        // one pass per image index i_a along the sweep axis: coefficient
+        // components without the axis phases (sweep_kernels.cu)
+        if (N >= (1 << 30)) throw Fail{FFTPIM_VALUE, "sweep plans need fewer than 2^30 sources"};
+        P->sw_comp = dalloc<cplx>(P, (int64_t)P->sw_ncomp * npairs);
+        for (int j = 0; j < P->sw_ncomp; ++j) {
+            ImageSet imj = im;
+            make_images(pr, pr.kshift, imj, P->sw_axis, j - pr.i_d);
+            PairGeom pgj = pg;
+            code_phases(pr, pr.kshift, pgj, P->sw_axis);
+            launch_code_tables(tb, pg.ncodes, pgj, imj, tables, tab_total, s);
+            pa.coef = P->sw_comp + (int64_t)j * npairs;
+            pa.coef_r = nullptr;
+            launch_pairs_fill(pgj, imj, tb, pa, s);
+            pa.pair_codeid = nullptr;   // written once
+        }
+        signed char ca[27] = {0};
+        for (int c = 0; c < pg.ncodes; ++c) ca[c] = pg.code[c][P->sw_axis];
+        launch_sweep_pack_src(P->pair_src, P->pair_codeid, ca, npairs, s);
+        P->info.real_coefficients = 0;
+    } else {
+        launch_code_tables(tb, pg.ncodes, pg, im, tables, tab_total, s);
+        if (P->npsp)
+            P->pair_coef_r = dalloc<double>(P, npairs);
+        else
+            P->pair_coef = dalloc<cplx>(P, npairs);
+        P->info.real_coefficients = P->npsp ? 1 : 0;
+        pa.coef = P->pair_coef;
+        pa.coef_r = P->pair_coef_r;
+        launch_pairs_fill(pg, im, tb, pa, s);
+    }
     P->n_tiles = (npairs + CORR_TILE - 1) / CORR_TILE;
-    P->head_bits = dalloc<unsigned>(P, (npairs + 31) / 32 + 8);
-    P->seg_first = dalloc<int64_t>(P, Mown + 1);
-    P->seg_base = dalloc<int64_t>(P, P->n_tiles);
-    {
+    if (!P->sweep) {   // the batched sweep K4 walks pair_ptr rows directly
+        P->head_bits = dalloc<unsigned>(P, (npairs + 31) / 32 + 8);
+        P->seg_first = dalloc<int64_t>(P, Mown + 1);
+        P->seg_base = dalloc<int64_t>(P, P->n_tiles);
         int64_t* spans = dalloc<int64_t>(P, Mown + 1);
         build_corr_metadata(P->pair_ptr, Mown, npairs, P->n_tiles, P->head_bits, P->seg_first, P->seg_base, spans,
                             &P->n_segments, s);
         dfree(P, spans);
+        P->seg_val = dalloc<cplx>(P, P->n_segments);
     }
-    P->seg_val = dalloc<cplx>(P, P->n_segments);
     check_status(P, "correction coefficients");
     CK(cudaStreamSynchronize(s));
     dfree(P, tables);
@@ -923,54 +1026,39 @@ void build(FftpimPlan* P) {
     }
 
     // ---- far kernel (farzone.py:100-121, pgf.py:450-462)
-    {
-        std::vector<double> axes;
-        double zmin = 1e300, zmax = -1e300;
-        for (int a = 0; a < 3; ++a) {
-            int n = fdims[a];
-            double shift = P->far_og.origin[a] - P->far_sg.origin[a];
-            if (n == 1) {
-                axes.push_back(shift);
-                if (a == 2) zmin = zmax = shift;
-            } else {
-                for (int l = -(n - 1); l < n; ++l) {
-                    double v = (double)l * fh[a] + shift;
-                    axes.push_back(v);
-                    if (a == 2) {
-                        zmin = std::min(zmin, v);
-                        zmax = std::max(zmax, v);
-                    }
-                }
+    P->far_kernel = dalloc<cplx>(P, prod3(P->far_kdims));
+    P->info.kernel_terms = tabulate_far(P, pr.kshift, im, P->far_kernel, s);
+    // ---- sweep: kernel_hat and far kernel per excitation
+    if (P->sweep) {
+        const int64_t nk = prod3(P->far_kdims);
+        P->sw_khat = dalloc<cplx>(P, (int64_t)P->sw_E * P->n_fft);
+        P->sw_far = dalloc<cplx>(P, (int64_t)P->sw_E * nk);
+        const int NS = P->sw_ncomp + 2;
+        std::vector<cplx> omega((size_t)P->sw_E * NS);
+        for (int e = 0; e < P->sw_E; ++e) {
+            double ks[3][2];
+            for (int a = 0; a < 3; ++a) {
+                ks[a][0] = pr.kshift[a][0];
+                ks[a][1] = pr.kshift[a][1];
+            }
+            ks[P->sw_axis][0] = P->sw_k[2 * e];
+            ks[P->sw_axis][1] = P->sw_k[2 * e + 1];
+            ImageSet ime = im;
+            make_images(pr, ks, ime);
+            tabulate_khat(P, dims, h, ime, P->sw_khat + (int64_t)e * P->n_fft, s);
+            P->info.kernel_terms = std::max(P->info.kernel_terms, tabulate_far(P, ks, ime, P->sw_far + (int64_t)e * nk, s));
+            const std::complex<double> kl = std::complex<double>(ks[P->sw_axis][0], ks[P->sw_axis][1]) * pr.L[P->sw_axis];
+            for (int k = 0; k < NS; ++k) {
+                const double m = (double)(k - 1 - pr.i_d);
+                const std::complex<double> w = std::exp(std::complex<double>(0.0, -1.0) * m * kl);
+                omega[(size_t)e * NS + k] = cplx{w.real(), w.imag()};
             }
         }
-        double* d_axes = dalloc<double>(P, (int64_t)axes.size());
-        CK(cudaMemcpyAsync(d_axes, axes.data(), sizeof(double) * axes.size(), cudaMemcpyHostToDevice, s));
-        FarSeriesParams fp{};
-        fp.dim = pr.dim;
-        fp.npsp = P->npsp;
-        for (int a = 0; a < 3; ++a) {
-            fp.L[a] = pr.L[a];
-            fp.ks_re[a] = pr.kshift[a][0];
-            fp.ks_im[a] = pr.kshift[a][1];
-        }
-        fp.k0_re = pr.k0[0];
-        fp.k0_im = pr.k0[1];
-        fp.tol = pr.series_tol;
-        fp.cutoff = std::log(1.0 / pr.series_tol) + 8.0;
-        fp.sep = im.sep_tol;
-        fp.wood = 1e-8 * 2.0 * M_PI / maxLp;
-        fp.zmin = zmin;
-        fp.zmax = zmax;
-        fp.max_terms = 1000000;
-        fp.max_layers = 200000;
-        GLTable gl = gauss_laguerre_half();
-        P->far_kernel = dalloc<cplx>(P, prod3(P->far_kdims));
-        launch_far_series(d_axes, P->far_kdims, fp, im, gl, P->far_kernel, P->status, s);
-        check_status(P, "far kernel tabulation");
-        DevStatus st;
-        CK(cudaMemcpy(&st, P->status, sizeof(st), cudaMemcpyDeviceToHost));
-        P->info.kernel_terms = st.kernel_terms;
-        dfree(P, d_axes);
+        P->sw_omega = dalloc<cplx>(P, (int64_t)P->sw_E * NS);
+        CK(cudaMemcpyAsync(P->sw_omega, omega.data(), sizeof(cplx) * omega.size(), cudaMemcpyHostToDevice, s));
+        P->sw_qt = dalloc<cplx>(P, N * P->sw_E);
+        P->sw_corr = dalloc<cplx>(P, Mown * P->sw_E);
+        CK(cudaStreamSynchronize(s));
     }
     // far evaluation scratch
     {
@@ -1463,7 +1551,13 @@ void fftpim_count_launch(int n) { g_launches += n; }
 
 extern "C" {
 
-static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool sharded, FftpimPlan** out) {
+struct SweepSpec {
+    int axis, E;
+    const double* k;   // (E, 2)
+};
+
+static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool sharded, FftpimPlan** out,
+                             const SweepSpec* sw = nullptr) {
     if (!p || !out) return fail(Fail{FFTPIM_VALUE, "null argument"});
     *out = nullptr;
     auto t0 = std::chrono::steady_clock::now();
@@ -1473,6 +1567,20 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
         P->rank = rank;
         P->sharded = sharded;
         P->prob = *p;
+        if (sw) {
+            if (sw->axis < 0 || sw->axis >= p->dim) throw Fail{FFTPIM_VALUE, "sweep axis must be a periodic axis"};
+            if (sw->E < 1 || sw->E > 64) throw Fail{FFTPIM_VALUE, "a sweep plan holds 1..64 excitations"};
+            if (p->regime == FFTPIM_NPSP) throw Fail{FFTPIM_VALUE, "NPSP problems have no phase shift to sweep"};
+            if (p->i_d > 2) throw Fail{FFTPIM_VALUE, "i_d > 2 is not supported by this build"};
+            P->sweep = true;
+            P->sw_axis = sw->axis;
+            P->sw_E = sw->E;
+            P->sw_ncomp = 2 * p->i_d + 1;
+            P->sw_k.assign(sw->k, sw->k + 2 * sw->E);
+            // the base geometry carries excitation 0's shift
+            P->prob.kshift[sw->axis][0] = sw->k[0];
+            P->prob.kshift[sw->axis][1] = sw->k[1];
+        }
         P->device = p->device;
         P->use_graphs = getenv("FFTPIM_NO_GRAPHS") == nullptr;
         memset(&P->info, 0, sizeof(P->info));
@@ -1515,6 +1623,72 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
 }
 
 int fftpim_plan_create(const FftpimProblem* p, FftpimPlan** out) { return plan_create_shard(p, 1, 0, false, out); }
+
+int fftpim_sweep_create(const FftpimProblem* p, int32_t axis, int32_t n_exc, const double* kshift_axis,
+                        FftpimPlan** out) {
+    if (!kshift_axis) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    SweepSpec sw{axis, n_exc, kshift_axis};
+    return plan_create_shard(p, 1, 0, false, out, &sw);
+}
+
+// One sweep evaluation: the batched K4 for all excitations, then per excitation
+// the permutation, far chain, K1, the FFT stages with its kernel_hat and the
+// observer pass taking its K4 sums from sw_corr.
+static void sweep_evaluate(FftpimPlan* P, const double* q, double* u, cudaStream_t s) {
+    const int E = P->sw_E;
+    launch_sweep_permute((const cplx*)q, P->src_perm, P->N, E, P->sw_qt, s);
+    launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, E, P->sw_omega,
+                      P->sw_corr, P->M, s);
+    const int64_t nk = prod3(P->far_kdims);
+    if (!P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
+    for (int e = 0; e < E; ++e) {
+        EvalArgs a = eval_args(P, q + 2 * (int64_t)e * P->N, u + 2 * (int64_t)e * P->M, FFTPIM_ALL);
+        a.khat = P->sw_khat + (int64_t)e * P->n_fft;
+        a.far_kernel = P->sw_far + (int64_t)e * nk;
+        a.sw_corr = P->sw_corr;
+        a.sw_E = E;
+        a.sw_e = e;
+        launch_permute_q(a, s);
+        launch_far_project(a, s);
+        launch_far_sum(a, s);
+        launch_near_project(a, s);
+        if (P->custom_fft) {
+            for (int k = 0; k < 5; ++k) {
+                if (!P->stage_on[k]) continue;
+                FftStage st = P->stage[k];
+                if (st.spec) st.spec = a.khat;
+                launch_fft_stage(st, s);
+            }
+        } else {
+            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+            launch_spectrum_mul(a, s);
+            CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+            fftpim_count_launch(2);
+        }
+        launch_observers(a, s);
+    }
+    CK(cudaGetLastError());
+}
+
+int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* stream) {
+    if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (!plan->sweep) return fail(Fail{FFTPIM_VALUE, "not a sweep plan (use fftpim_plan_evaluate)"});
+    if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
+    try {
+        CK(cudaSetDevice(plan->device));
+        sweep_evaluate(plan, q, u, (cudaStream_t)stream);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_sweep_info(const FftpimPlan* plan, int32_t* axis, int32_t* n_exc) {
+    if (!plan || !axis || !n_exc) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    *axis = plan->sweep ? plan->sw_axis : -1;
+    *n_exc = plan->sweep ? plan->sw_E : 0;
+    return FFTPIM_OK;
+}
 
 int fftpim_nccl_unique_id(void* out, int64_t bytes) {
     if (!out || bytes < (int64_t)sizeof(ncclUniqueId)) return fail(Fail{FFTPIM_VALUE, "need a 128-byte buffer"});
@@ -1592,6 +1766,7 @@ void fftpim_group_destroy(FftpimGroup* g) {
 
 int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts, void* stream) {
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});
     if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
         evaluate(plan, q, u, batch, parts, (cudaStream_t)stream);
@@ -1603,6 +1778,7 @@ int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t b
 
 int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts) {
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});
     try {
         CK(cudaSetDevice(plan->device));
         cudaStream_t s = plan->build_stream;
@@ -1673,6 +1849,7 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
 int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t parts, void* stream,
                         double* stage_ms) {
     if (!plan || !q || !u || !stage_ms) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "stage profiles are for single-excitation plans"});
     cudaEvent_t ev[FFTPIM_N_STAGES + 1] = {};
     try {
         CK(cudaSetDevice(plan->device));
@@ -1748,7 +1925,8 @@ int fftpim_plan_export(const FftpimPlan* cplan, int32_t which, void* dst, int64_
             CK(cudaMemcpy(psrc.data(), P->pair_src, sizeof(int) * npairs, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(sperm.data(), P->src_perm, sizeof(int) * N, cudaMemcpyDeviceToHost));
             int* o = (int*)dst;
-            for (int64_t k = 0; k < npairs; ++k) o[k] = sperm[psrc[order[k]]];
+            const int mask = P->sweep ? 0x3fffffff : -1;   // sweep plans pack the axis code in bits 30-31
+            for (int64_t k = 0; k < npairs; ++k) o[k] = sperm[psrc[order[k]] & mask];
         } else if (which == FFTPIM_PAIR_CODE) {
             need(npairs * 3);
             std::vector<unsigned char> cid(npairs);
@@ -1759,6 +1937,7 @@ int fftpim_plan_export(const FftpimPlan* cplan, int32_t which, void* dst, int64_
                 for (int a = 0; a < 3; ++a) o[3 * k + a] = P->pg.code[cid[order[k]]][a];
         } else {
             need(npairs * 16);
+            if (P->sweep) throw Fail{FFTPIM_VALUE, "sweep plans hold coefficient components, not coefficients"};
             double* o = (double*)dst;
             if (P->pair_coef_r) {
                 std::vector<double> c(npairs);

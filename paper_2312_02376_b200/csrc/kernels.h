@@ -132,6 +132,8 @@ struct EvalArgs {
     const cplx* far_q;          // sources projected onto the far grid (own range for shards)
     int64_t far_n;
     cplx* obs_pre;              // far + K4 fix-up per sorted observer (split observer pass)
+    const cplx* sw_corr;        // sweep: K4 sums (M, E) replace the segment fix-up
+    int sw_E, sw_e;
     int parts;
 };
 void launch_permute_q(const EvalArgs& a, cudaStream_t s);
@@ -151,6 +153,16 @@ void launch_observers(const EvalArgs& a, cudaStream_t s, int mode = 0);   // 0 f
 // ---- pruned column-FFT stages (fft_kernels.cu)
 size_t fft_stage_smem(const FftStage& st);
 void launch_fft_stage(const FftStage& st, cudaStream_t s);
+
+// ---- batched excitation sweep (sweep_kernels.cu)
+struct SweepCodeAxis {
+    int c[27];                  // code component along the sweep axis per code id
+};
+void launch_sweep_pack_src(int* pair_src, const unsigned char* codeid, const signed char* code_axis, int64_t P,
+                           cudaStream_t s);
+void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, cplx* qt, cudaStream_t s);
+void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp, int ncomp, int64_t P,
+                       const cplx* qt, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s);
 
 // ---- correction matvec (corr_kernels.cu)
 #define CORR_TILE 256

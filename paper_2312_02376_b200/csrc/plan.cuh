@@ -213,6 +213,19 @@ struct FftpimPlan {
     cudaStream_t gstream = nullptr;                  // graph replay stream for legacy-stream callers
     cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
 
+    // batched excitation sweep: E phase shifts differing only
+    // along periodic axis sw_axis; one pair list with 2 i_d + 1 phase components
+    bool sweep = false;
+    int sw_axis = 0, sw_E = 0, sw_ncomp = 0;
+    std::vector<double> sw_k;          // (E, 2) kshift component along sw_axis
+    cplx* sw_comp = nullptr;           // (ncomp, P) coefficient components
+    cplx* sw_khat = nullptr;           // (E, n_fft) kernel_hat per excitation
+    cplx* sw_far = nullptr;            // (E, nk) far kernel per excitation
+    cplx* sw_omega = nullptr;          // (E, ncomp + 2) exp(-j m k_e L), m = -(i_d+1) .. i_d+1
+    cplx* sw_qt = nullptr;             // (N, E) sorted charges, excitation fastest
+    cplx* sw_corr = nullptr;           // (M, E) batched K4 sums, excitation fastest
+    int64_t sw_batch_cap = 0;
+
     DevStatus* status = nullptr;
     int64_t device_bytes = 0;
     std::vector<void*> allocations;
