@@ -122,6 +122,10 @@ FFTPIM_API int fftpim_sweep_create(const FftpimProblem* p, int32_t axis, int32_t
  * complex128 DEVICE pointers (16-byte aligned), stream ordered. */
 FFTPIM_API int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* stream);
 
+/* Device milliseconds of one sweep evaluation: ms[0] the batched precorrection
+ * (with its transposed permutation), ms[1] the rest (per-excitation chains). */
+FFTPIM_API int fftpim_sweep_profile(FftpimPlan* plan, const double* q, double* u, void* stream, double* ms);
+
 /* axis and excitation count of a sweep plan (-1, 0 for ordinary plans). */
 FFTPIM_API int fftpim_sweep_info(const FftpimPlan* plan, int32_t* axis, int32_t* n_exc);
 

@@ -1683,6 +1683,37 @@ int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* st
     }
 }
 
+int fftpim_sweep_profile(FftpimPlan* plan, const double* q, double* u, void* stream, double* ms) {
+    if (!plan || !q || !u || !ms) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (!plan->sweep) return fail(Fail{FFTPIM_VALUE, "not a sweep plan"});
+    cudaEvent_t ev[3] = {};
+    try {
+        CK(cudaSetDevice(plan->device));
+        cudaStream_t s = (cudaStream_t)stream;
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        FftpimPlan* P = plan;
+        CK(cudaEventRecord(ev[0], s));
+        launch_sweep_permute((const cplx*)q, P->src_perm, P->N, P->sw_E, P->sw_qt, s);
+        launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, P->sw_E,
+                          P->sw_omega, P->sw_corr, P->M, s);
+        CK(cudaEventRecord(ev[1], s));
+        sweep_evaluate(P, q, u, s);
+        CK(cudaEventRecord(ev[2], s));
+        CK(cudaEventSynchronize(ev[2]));
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        ms[0] = a;          // batched K4 (with the transposed permutation)
+        ms[1] = b - a;      // everything else of one sweep evaluation
+        for (auto& e : ev) cudaEventDestroy(e);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        return fail(f);
+    }
+}
+
 int fftpim_sweep_info(const FftpimPlan* plan, int32_t* axis, int32_t* n_exc) {
     if (!plan || !axis || !n_exc) return fail(Fail{FFTPIM_VALUE, "null argument"});
     *axis = plan->sweep ? plan->sw_axis : -1;

@@ -50,8 +50,9 @@ void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, cplx
 }
 
 // warp per sorted observer; lane l owns excitations l and l + 32 (E <= 64).
-// Pairs are taken 32 at a time: lane k loads pair k's packed source and
-// components (coalesced), then the warp walks the 32 pairs with shuffles.
+// Pairs are taken 32 at a time: lane k stages pair k's packed source and
+// components in shared memory (coalesced loads), then the warp walks the 32
+// pairs reading them as broadcasts, four pairs' q rows in flight at a time.
 template <int NC, bool TWO>
 __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ ptr, const int* __restrict__ psrc,
                                                     const cplx* __restrict__ comp, int64_t P,
@@ -59,7 +60,9 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
                                                     const cplx* __restrict__ omega, cplx* __restrict__ corr,
                                                     int64_t M) {
     constexpr int NS = NC + 2;   // powers m = -(h+1) .. h+1, h = NC / 2
-    const int lane = threadIdx.x & 31;
+    __shared__ cplx s_b[8][NC][32];
+    __shared__ int s_v[8][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (i >= M) return;
     const int e0 = lane, e1 = lane + 32;
@@ -70,29 +73,21 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
     const int64_t p0 = ptr[i], p1 = ptr[i + 1];
     for (int64_t b = p0; b < p1; b += 32) {
         const int cnt = (int)min((int64_t)32, p1 - b);
-        int my = 0;
-        double ar[NC], ai[NC];
+        __syncwarp();
         if (lane < cnt) {
-            my = psrc[b + lane];
+            s_v[wid][lane] = psrc[b + lane];
 #pragma unroll
-            for (int j = 0; j < NC; ++j) {
-                const cplx c = comp[(int64_t)j * P + b + lane];
-                ar[j] = c.re;
-                ai[j] = c.im;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < NC; ++j) ar[j] = ai[j] = 0.0;
+            for (int j = 0; j < NC; ++j) s_b[wid][j][lane] = comp[(int64_t)j * P + b + lane];
         }
-        // four pairs per step: their q loads issue together
+        __syncwarp();
         for (int k0 = 0; k0 < cnt; k0 += 4) {
             int v[4];
             cplx q0[4], q1[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                v[u] = __shfl_sync(0xffffffffu, my, (k0 + u) & 31);
-                const cplx* qrow = qt + (int64_t)(v[u] & 0x3fffffff) * E;
                 const bool in = k0 + u < cnt;
+                v[u] = in ? s_v[wid][k0 + u] : 0;
+                const cplx* qrow = qt + (int64_t)(v[u] & 0x3fffffff) * E;
                 q0[u] = (in && ok0) ? qrow[e0] : mk(0.0);
                 q1[u] = (in && ok1) ? qrow[e1] : mk(0.0);
             }
@@ -100,23 +95,20 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
             for (int u = 0; u < 4; ++u) {
                 if (k0 + u >= cnt) break;
                 const int ca = (v[u] >> 30) & 3;   // code along the axis + 1 (warp-uniform)
-                double br[NC], bi[NC];
+                cplx bj[NC];
 #pragma unroll
-                for (int j = 0; j < NC; ++j) {
-                    br[j] = __shfl_sync(0xffffffffu, ar[j], k0 + u);
-                    bi[j] = __shfl_sync(0xffffffffu, ai[j], k0 + u);
-                }
+                for (int j = 0; j < NC; ++j) bj[j] = s_b[wid][j][k0 + u];
                 // S[ca + j] += B_j q
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     if (ca != c) continue;
 #pragma unroll
                     for (int j = 0; j < NC; ++j) {
-                        s0r[c + j] += br[j] * q0[u].re - bi[j] * q0[u].im;
-                        s0i[c + j] += br[j] * q0[u].im + bi[j] * q0[u].re;
+                        s0r[c + j] += bj[j].re * q0[u].re - bj[j].im * q0[u].im;
+                        s0i[c + j] += bj[j].re * q0[u].im + bj[j].im * q0[u].re;
                         if (TWO) {
-                            s1r[c + j] += br[j] * q1[u].re - bi[j] * q1[u].im;
-                            s1i[c + j] += br[j] * q1[u].im + bi[j] * q1[u].re;
+                            s1r[c + j] += bj[j].re * q1[u].re - bj[j].im * q1[u].im;
+                            s1i[c + j] += bj[j].re * q1[u].im + bj[j].im * q1[u].re;
                         }
                     }
                 }

@@ -61,6 +61,12 @@ class SweepPlan:
         """Raw device pointers: q (E, N) and u (E, M) complex128."""
         nat.check(self._lib.fftpim_sweep_evaluate(self._h, q_ptr, u_ptr, stream))
 
+    def profile(self, q_ptr: int, u_ptr: int, stream: int = 0) -> dict:
+        """Device ms of one sweep: the batched precorrection and the rest."""
+        ms = (C.c_double * 2)()
+        nat.check(self._lib.fftpim_sweep_profile(self._h, q_ptr, u_ptr, stream, ms))
+        return {"corr_sweep": ms[0], "per_excitation_chains": ms[1]}
+
     def evaluate(self, Q):
         """U[e] = potential of excitation e.  CUDA tensor in -> CUDA tensor out;
         numpy in -> numpy out (through device copies)."""
