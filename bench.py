@@ -383,8 +383,8 @@ def run_slab(args):
 
 
 def run_sweep(args):
-    """C5: the 64-excitation sweep.  Excitations are sharded over the ranks in
-    contiguous blocks; each rank holds one SweepPlan (shared geometry and pair
+    """C5: the 64-excitation sweep.  Excitations are sharded over the ranks
+    (sharding.excitation_shard); each rank holds one SweepPlan (shared geometry and pair
     list, phase-factorised coefficients, batched precorrection) and evaluates its
     block; no collective in the loop.  Total work fixed: 'scaling': 'strong'."""
     import torch
@@ -398,8 +398,9 @@ def run_sweep(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = CONFIGS[args.config]
     pos, qall = make_inputs(args.config)
+    from paper_2312_02376_b200.sharding import excitation_shard
     E = w.excitations
-    es = list(range(rank * E // world, (rank + 1) * E // world))
+    es = excitation_shard(E, world, rank)
     cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=c5_kshift(es[0]),
                                regime=fp.Regime(w.regime))
     t0 = time.perf_counter()
@@ -469,7 +470,7 @@ def run_sweep(args):
             "data": "synthetic (seeded, workloads.py)",
             "config": {"workload": w.name, "N": w.n_points, "excitations": E, "near_grid": list(w.near_grid),
                        "near_order": w.near_order, "regime": w.regime, "pairs": P,
-                       "parallelism": f"excitation blocks x{world} (sweep plans: phase-factorised pairs)",
+                       "parallelism": f"excitation shards x{world} (sweep plans: phase-factorised pairs)",
                        "step": f"one sweep evaluation of {len(es)} excitations per rank",
                        "l2": f"working set > L2 (coefficient components {P * 16 * nc / 1e9:.0f} GB)"},
             "rel_l2_vs_reference": rel, "rel_l2_basis": basis,
