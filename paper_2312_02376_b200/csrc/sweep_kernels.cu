@@ -11,6 +11,8 @@
 // warp per observer, lanes own excitations, per-power accumulators
 // S_m = sum_pairs B_j q_e[src] (m = c_a + j - i_d), and at the row end
 // corr_e = sum_m omega_e^m S_m.  Fixed order, no atomics.
+#include <cstdlib>
+
 #include "geom.cuh"
 #include "kernels.h"
 
@@ -53,7 +55,10 @@ void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, cplx
 // Pairs are taken 32 at a time: lane k stages pair k's packed source and
 // components in shared memory (coalesced loads), then the warp walks the 32
 // pairs reading them as broadcasts, four pairs' q rows in flight at a time.
-template <int NC, bool TWO>
+#ifndef SWEEP_U   // pairs whose q rows are in flight together
+#define SWEEP_U 2
+#endif
+template <int NC, bool TWO, bool HALVES>
 __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ ptr, const int* __restrict__ psrc,
                                                     const cplx* __restrict__ comp, int64_t P,
                                                     const cplx* __restrict__ qt, int E,
@@ -63,9 +68,10 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
     __shared__ cplx s_b[8][NC][32];
     __shared__ int s_v[8][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t i = HALVES ? gw >> 1 : gw;
     if (i >= M) return;
-    const int e0 = lane, e1 = lane + 32;
+    const int e0 = HALVES ? lane + 32 * (int)(gw & 1) : lane, e1 = lane + 32;
     const bool ok0 = e0 < E, ok1 = TWO && e1 < E;
     double s0r[NS], s0i[NS], s1r[NS], s1i[NS];
 #pragma unroll
@@ -80,11 +86,11 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
             for (int j = 0; j < NC; ++j) s_b[wid][j][lane] = comp[(int64_t)j * P + b + lane];
         }
         __syncwarp();
-        for (int k0 = 0; k0 < cnt; k0 += 4) {
-            int v[4];
-            cplx q0[4], q1[4];
+        for (int k0 = 0; k0 < cnt; k0 += SWEEP_U) {
+            int v[SWEEP_U];
+            cplx q0[SWEEP_U], q1[SWEEP_U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < SWEEP_U; ++u) {
                 const bool in = k0 + u < cnt;
                 v[u] = in ? s_v[wid][k0 + u] : 0;
                 const cplx* qrow = qt + (int64_t)(v[u] & 0x3fffffff) * E;
@@ -92,7 +98,7 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
                 q1[u] = (in && ok1) ? qrow[e1] : mk(0.0);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < SWEEP_U; ++u) {
                 if (k0 + u >= cnt) break;
                 const int ca = (v[u] >> 30) & 3;   // code along the axis + 1 (warp-uniform)
                 cplx bj[NC];
@@ -141,11 +147,27 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
 void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp, int ncomp, int64_t P,
                        const cplx* qt, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s) {
     if (M == 0) return;
-    const int blocks = nblk(M * 32, 256);
+    // E > 32: two warps per observer (one per 32 excitations, adjacent in the
+    // block so the second reads the pair data from L1) or one warp with two
+    // excitations per lane (default; measured faster, FFTPIM_SWEEP_HALVES=1 for the other)
+    static const bool halves = [] {
+        const char* e = getenv("FFTPIM_SWEEP_HALVES");
+        return e && e[0] == '1';
+    }();
     const bool two = E > 32;
-#define KS(NC)                                                                                       \
-    if (two) k_corr_sweep<NC, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M); \
-    else k_corr_sweep<NC, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
+    if (two && halves) {
+        const int blocks = nblk(M * 64, 256);
+        if (ncomp == 3)
+            k_corr_sweep<3, false, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
+        else
+            k_corr_sweep<5, false, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
+        fftpim_count_launch();
+        return;
+    }
+    const int blocks = nblk(M * 32, 256);
+#define KS(NC)                                                                                              \
+    if (two) k_corr_sweep<NC, true, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M); \
+    else k_corr_sweep<NC, false, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
     if (ncomp == 3) {
         KS(3)
     } else {
