@@ -122,8 +122,17 @@ FFTPIM_API int fftpim_sweep_create(const FftpimProblem* p, int32_t axis, int32_t
  * complex128 DEVICE pointers (16-byte aligned), stream ordered. */
 FFTPIM_API int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* stream);
 
-/* Device milliseconds of one sweep evaluation: ms[0] the batched precorrection
- * (with its transposed permutation), ms[1] the rest (per-excitation chains). */
+/* Same with HOST q (E, n_src) / u (E, n_obs) (pinned or pageable), synchronous:
+ * excitation e's upload overlaps the chains of the excitations before it, the
+ * batched precorrection starts once every charge vector is resident, one
+ * download at the end.  This is the call a reference-side binding makes for a
+ * sweep (the reference evaluates each excitation with SolvePlan.evaluate,
+ * solver.py:24-25). */
+FFTPIM_API int fftpim_sweep_evaluate_host(FftpimPlan* plan, const double* q, double* u);
+
+/* Device milliseconds: ms[0] the batched precorrection alone (with its
+ * transposed permutation), ms[1] one whole sweep evaluation (the per-excitation
+ * chains overlap the batched precorrection). */
 FFTPIM_API int fftpim_sweep_profile(FftpimPlan* plan, const double* q, double* u, void* stream, double* ms);
 
 /* axis and excitation count of a sweep plan (-1, 0 for ordinary plans). */

@@ -52,7 +52,7 @@ EXPORTED = ("fftpim_plan_create", "fftpim_plan_evaluate", "fftpim_plan_evaluate_
             "fftpim_plan_destroy", "fftpim_last_error", "fftpim_launch_count", "fftpim_plan_profile",
             "fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
             "fftpim_group_destroy", "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info",
-            "fftpim_sweep_profile")
+            "fftpim_sweep_profile", "fftpim_sweep_evaluate_host")
 N_STAGES = 9
 STAGES = ("permute_q", "far_project", "far_sum", "near_project", "fft_forward", "spectrum_mul",
           "fft_inverse", "corr_matvec", "observers")
@@ -94,8 +94,10 @@ def load(path: str = LIB_PATH):
     lib.fftpim_sweep_evaluate.argtypes = [vp, vp, vp, vp]
     lib.fftpim_sweep_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     lib.fftpim_sweep_profile.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_double)]
+    lib.fftpim_sweep_evaluate_host.argtypes = [vp, vp, vp]
     for name in ("fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
-                 "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info", "fftpim_sweep_profile"):
+                 "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info", "fftpim_sweep_profile",
+                 "fftpim_sweep_evaluate_host"):
         getattr(lib, name).restype = C.c_int
     lib.fftpim_last_error.restype = C.c_char_p
     lib.fftpim_launch_count.restype = C.c_int64

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256, OBS_MINB) k_observers(EvalArgs a) {
     const bool active = i < a.M;
     const int64_t ii = active ? i : a.M - 1;
     double ar = 0.0, ai = 0.0;
-    if ((a.parts & FFTPIM_NEAR) && MODE != 2 && active && sub == OBS_LPO - 1) {
+    if ((a.parts & FFTPIM_NEAR) && MODE != 2 && active && sub == OBS_LPO - 1 && a.sw_e >= 0) {
         // the observer's K4 segments, fetched by the last lane up front so the
         // dependent pointer chain overlaps the interpolation gathers
         const cplx c = a.sw_corr ? a.sw_corr[i * a.sw_E + a.sw_e] : corr_of_row(a, i);

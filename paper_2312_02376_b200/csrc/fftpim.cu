@@ -1631,42 +1631,63 @@ int fftpim_sweep_create(const FftpimProblem* p, int32_t axis, int32_t n_exc, con
     return plan_create_shard(p, 1, 0, false, out, &sw);
 }
 
-// One sweep evaluation: the batched K4 for all excitations, then per excitation
-// the permutation, far chain, K1, the FFT stages with its kernel_hat and the
-// observer pass taking its K4 sums from sw_corr.
-static void sweep_evaluate(FftpimPlan* P, const double* q, double* u, cudaStream_t s) {
+// One sweep evaluation.  The batched K4 for all excitations (FP64-bound) runs
+// on the low-priority stream while the per-excitation chains (permutation, far
+// chain, K1, the FFT stages with the excitation's kernel_hat, the observer pass
+// without the K4 term -- memory/latency-bound) run on the high-priority stream;
+// after both join, one pass adds the K4 sums to every potential.
+// `ready` (host entry): event e marks excitation e's charges resident; chain e
+// waits for it and the batched K4 for the last one.
+static void sweep_evaluate(FftpimPlan* P, const double* q, double* u, cudaStream_t s,
+                           const cudaEvent_t* ready = nullptr) {
     const int E = P->sw_E;
-    launch_sweep_permute((const cplx*)q, P->src_perm, P->N, E, P->sw_qt, s);
+    const bool serial = P->serial_sweep_required;
+    cudaStream_t sn = serial ? s : P->aux[0], sc = serial ? s : P->aux[1];
+    if (!serial) {
+        CK(cudaEventRecord(P->ev_fork, s));
+        CK(cudaStreamWaitEvent(sn, P->ev_fork, 0));
+        CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
+    }
+    if (ready) CK(cudaStreamWaitEvent(sc, ready[E - 1], 0));
+    launch_sweep_permute((const cplx*)q, P->src_perm, P->N, E, P->sw_qt, sc);
     launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, E, P->sw_omega,
-                      P->sw_corr, P->M, s);
+                      P->sw_corr, P->M, sc);
     const int64_t nk = prod3(P->far_kdims);
-    if (!P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
+    if (!P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, sn));
     for (int e = 0; e < E; ++e) {
         EvalArgs a = eval_args(P, q + 2 * (int64_t)e * P->N, u + 2 * (int64_t)e * P->M, FFTPIM_ALL);
         a.khat = P->sw_khat + (int64_t)e * P->n_fft;
         a.far_kernel = P->sw_far + (int64_t)e * nk;
-        a.sw_corr = P->sw_corr;
+        a.sw_corr = nullptr;
         a.sw_E = E;
-        a.sw_e = e;
-        launch_permute_q(a, s);
-        launch_far_project(a, s);
-        launch_far_sum(a, s);
-        launch_near_project(a, s);
+        a.sw_e = -1;   // the K4 term is added by launch_sweep_add_corr
+        if (ready) CK(cudaStreamWaitEvent(sn, ready[e], 0));
+        launch_permute_q(a, sn);
+        launch_far_project(a, sn);
+        launch_far_sum(a, sn);
+        launch_near_project(a, sn);
         if (P->custom_fft) {
             for (int k = 0; k < 5; ++k) {
                 if (!P->stage_on[k]) continue;
                 FftStage st = P->stage[k];
                 if (st.spec) st.spec = a.khat;
-                launch_fft_stage(st, s);
+                launch_fft_stage(st, sn);
             }
         } else {
             CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
-            launch_spectrum_mul(a, s);
+            launch_spectrum_mul(a, sn);
             CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
             fftpim_count_launch(2);
         }
-        launch_observers(a, s);
+        launch_observers(a, sn);
     }
+    if (!serial) {
+        CK(cudaEventRecord(P->ev_join[0], sn));
+        CK(cudaEventRecord(P->ev_join[1], sc));
+        CK(cudaStreamWaitEvent(s, P->ev_join[0], 0));
+        CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));
+    }
+    launch_sweep_add_corr((cplx*)u, P->sw_corr, P->obs_perm, P->M, E, s);
     CK(cudaGetLastError());
 }
 
@@ -1677,6 +1698,48 @@ int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* st
     try {
         CK(cudaSetDevice(plan->device));
         sweep_evaluate(plan, q, u, (cudaStream_t)stream);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        return fail(f);
+    }
+}
+
+int fftpim_sweep_evaluate_host(FftpimPlan* plan, const double* q, double* u) {
+    if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (!plan->sweep) return fail(Fail{FFTPIM_VALUE, "not a sweep plan (use fftpim_plan_evaluate_host)"});
+    try {
+        FftpimPlan* P = plan;
+        CK(cudaSetDevice(P->device));
+        const int E = P->sw_E;
+        cudaStream_t s = P->build_stream, sx = P->aux[2];
+        if (P->h_batch < E) {   // persistent device staging (E charge and potential vectors)
+            dfree(P, P->h_q);
+            dfree(P, P->h_u);
+            if (P->hgraph_exec) cudaGraphExecDestroy(P->hgraph_exec);
+            P->hgraph_exec = nullptr;
+            P->h_q = dalloc<double>(P, 2 * P->N * E);
+            P->h_u = dalloc<double>(P, 2 * P->M * E);
+            P->h_batch = E;
+        }
+        if ((int)P->sw_ready.size() < E) {
+            for (int e = (int)P->sw_ready.size(); e < E; ++e) {
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                P->sw_ready.push_back(ev);
+            }
+        }
+        // upload excitation by excitation on the copy stream; each chain starts
+        // as soon as its charges are resident
+        CK(cudaEventRecord(P->ev_fork, s));
+        CK(cudaStreamWaitEvent(sx, P->ev_fork, 0));
+        const size_t qb = sizeof(double) * 2 * P->N;
+        for (int e = 0; e < E; ++e) {
+            CK(cudaMemcpyAsync(P->h_q + 2 * P->N * e, q + 2 * P->N * e, qb, cudaMemcpyHostToDevice, sx));
+            CK(cudaEventRecord(P->sw_ready[e], sx));
+        }
+        sweep_evaluate(P, P->h_q, P->h_u, s, P->sw_ready.data());
+        CK(cudaMemcpyAsync(u, P->h_u, sizeof(double) * 2 * P->M * E, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         return FFTPIM_OK;
     } catch (const Fail& f) {
         return fail(f);
@@ -1703,8 +1766,8 @@ int fftpim_sweep_profile(FftpimPlan* plan, const double* q, double* u, void* str
         float a = 0.f, b = 0.f;
         CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
         CK(cudaEventElapsedTime(&b, ev[1], ev[2]));
-        ms[0] = a;          // batched K4 (with the transposed permutation)
-        ms[1] = b - a;      // everything else of one sweep evaluation
+        ms[0] = a;          // batched K4 alone (with the transposed permutation)
+        ms[1] = b;          // one whole (overlapped) sweep evaluation
         for (auto& e : ev) cudaEventDestroy(e);
         return FFTPIM_OK;
     } catch (const Fail& f) {
@@ -2023,6 +2086,7 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
     if (plan->ev_k1) cudaEventDestroy(plan->ev_k1);
     if (plan->ev_out) cudaEventDestroy(plan->ev_out);
     if (plan->gstream) cudaStreamDestroy(plan->gstream);
+    for (auto e : plan->sw_ready) cudaEventDestroy(e);
     for (auto e : plan->ev_join)
         if (e) cudaEventDestroy(e);
     if (plan->build_stream) cudaStreamDestroy(plan->build_stream);

@@ -133,7 +133,7 @@ struct EvalArgs {
     int64_t far_n;
     cplx* obs_pre;              // far + K4 fix-up per sorted observer (split observer pass)
     const cplx* sw_corr;        // sweep: K4 sums (M, E) replace the segment fix-up
-    int sw_E, sw_e;
+    int sw_E, sw_e;             // sw_e < 0: the observer pass leaves the K4 term out
     int parts;
 };
 void launch_permute_q(const EvalArgs& a, cudaStream_t s);
@@ -163,6 +163,7 @@ void launch_sweep_pack_src(int* pair_src, const unsigned char* codeid, const sig
 void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, cplx* qt, cudaStream_t s);
 void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp, int ncomp, int64_t P,
                        const cplx* qt, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s);
+void launch_sweep_add_corr(cplx* u, const cplx* corr, const int* obs_perm, int64_t M, int E, cudaStream_t s);
 
 // ---- correction matvec (corr_kernels.cu)
 #define CORR_TILE 256

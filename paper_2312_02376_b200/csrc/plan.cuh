@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include <string>
 #include <vector>
@@ -219,6 +220,8 @@ struct FftpimPlan {
     int sw_axis = 0, sw_E = 0, sw_ncomp = 0;
     std::vector<double> sw_k;          // (E, 2) kshift component along sw_axis
     cplx* sw_comp = nullptr;           // (ncomp, P) coefficient components
+    std::vector<cudaEvent_t> sw_ready;   // host entry: excitation e's charges uploaded
+    bool serial_sweep_required = getenv("FFTPIM_SWEEP_SERIAL") != nullptr;   // diagnostics: one stream
     cplx* sw_khat = nullptr;           // (E, n_fft) kernel_hat per excitation
     cplx* sw_far = nullptr;            // (E, nk) far kernel per excitation
     cplx* sw_omega = nullptr;          // (E, ncomp + 2) exp(-j m k_e L), m = -(i_d+1) .. i_d+1

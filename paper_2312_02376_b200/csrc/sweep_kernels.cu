@@ -176,3 +176,22 @@ void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp
 #undef KS
     fftpim_count_launch();
 }
+
+// u[e][obs_perm[i]] += corr[i][e]: the batched K4 sums into the potentials the
+// per-excitation observer passes wrote (thread per (observer, excitation),
+// excitation fastest: coalesced corr reads)
+__global__ void k_sweep_add_corr(cplx* __restrict__ u, const cplx* __restrict__ corr, const int* __restrict__ perm,
+                                 int64_t M, int E) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= M * E) return;
+    const int64_t i = t / E;
+    const int e = (int)(t - i * E);
+    cplx* d = u + (int64_t)e * M + perm[i];
+    *d = *d + corr[t];
+}
+
+void launch_sweep_add_corr(cplx* u, const cplx* corr, const int* obs_perm, int64_t M, int E, cudaStream_t s) {
+    if (M == 0) return;
+    k_sweep_add_corr<<<nblk(M * E, 256), 256, 0, s>>>(u, corr, obs_perm, M, E);
+    fftpim_count_launch();
+}

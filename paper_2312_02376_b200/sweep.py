@@ -62,24 +62,42 @@ class SweepPlan:
         nat.check(self._lib.fftpim_sweep_evaluate(self._h, q_ptr, u_ptr, stream))
 
     def profile(self, q_ptr: int, u_ptr: int, stream: int = 0) -> dict:
-        """Device ms of one sweep: the batched precorrection and the rest."""
+        """Device ms: the batched precorrection alone, and one whole sweep
+        evaluation (the per-excitation chains overlap the precorrection)."""
         ms = (C.c_double * 2)()
         nat.check(self._lib.fftpim_sweep_profile(self._h, q_ptr, u_ptr, stream, ms))
-        return {"corr_sweep": ms[0], "per_excitation_chains": ms[1]}
+        return {"corr_sweep": ms[0], "sweep_total": ms[1]}
 
-    def evaluate(self, Q):
-        """U[e] = potential of excitation e.  CUDA tensor in -> CUDA tensor out;
-        numpy in -> numpy out (through device copies)."""
+    def evaluate(self, Q, out=None):
+        """U[e] = potential of excitation e.  CUDA tensor in -> CUDA tensor out
+        (stream ordered on the current stream); host array in -> host array out
+        through fftpim_sweep_evaluate_host (uploads overlap the per-excitation
+        chains; pinned buffers, e.g. from torch's pin_memory(), transfer fastest).
+        `out`: optional host array (E, M) complex128 to write into."""
         import torch
-        on_dev = isinstance(Q, torch.Tensor) and Q.is_cuda
-        q = Q if on_dev else torch.from_numpy(np.ascontiguousarray(np.asarray(Q, dtype=np.complex128)))
-        if tuple(q.shape) != (self.n_excitations, self.n_sources):
-            raise ValueError(f"expected charges of shape {(self.n_excitations, self.n_sources)}, got {tuple(q.shape)}")
-        dev = torch.device("cuda", self.device)
-        qd = q.to(dev, dtype=torch.complex128).contiguous()
-        u = torch.empty((self.n_excitations, self.n_observers), dtype=torch.complex128, device=dev)
-        self.evaluate_into(qd.data_ptr(), u.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
-        return u if on_dev else u.cpu().numpy()
+        shape = (self.n_excitations, self.n_sources)
+        if isinstance(Q, torch.Tensor) and Q.is_cuda:
+            if tuple(Q.shape) != shape:
+                raise ValueError(f"expected charges of shape {shape}, got {tuple(Q.shape)}")
+            dev = torch.device("cuda", self.device)
+            qd = Q.to(dev, dtype=torch.complex128).contiguous()
+            u = torch.empty((self.n_excitations, self.n_observers), dtype=torch.complex128, device=dev)
+            self.evaluate_into(qd.data_ptr(), u.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+            return u
+        if isinstance(Q, torch.Tensor):
+            Q = Q.numpy()
+        q = np.asarray(Q)
+        if q.shape != shape:
+            raise ValueError(f"expected charges of shape {shape}, got {q.shape}")
+        if q.dtype != np.complex128 or not q.flags.c_contiguous:
+            q = np.ascontiguousarray(q, dtype=np.complex128)
+        if out is None:
+            out = np.empty((self.n_excitations, self.n_observers), dtype=np.complex128)
+        elif out.shape != (self.n_excitations, self.n_observers) or out.dtype != np.complex128 \
+                or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous complex128 array of shape (E, M)")
+        nat.check(self._lib.fftpim_sweep_evaluate_host(self._h, q.ctypes.data, out.ctypes.data))
+        return out
 
 
 def build_sweep_plan(cfg: PeriodicityConfig, box: TargetBox, src: SourcePointSet, obs: ObserverPointSet,

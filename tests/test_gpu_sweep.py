@@ -96,3 +96,28 @@ def test_sweep_c5_subset(fp):
                              fp.SolverParams(**w.params()))
         assert rel_l2(U[j], plan.evaluate(Q[j])) <= 1e-12
         del plan
+
+
+def test_sweep_device_and_host_entries_agree(fp):
+    """The device entry (caller stream, tensors) and the host entry (chunked
+    uploads overlapping the chains) give bitwise identical potentials, and
+    repeated sweeps are bitwise reproducible (fixed-order reductions only)."""
+    import torch
+    name = "p2_dyn"
+    case = SMALL_CASES[name]
+    pos, q, obs = case_inputs(name)
+    shifts = [complex(case["kshift"][0]) + 0.1 * e for e in range(40)]   # E > 32: two excitations per lane
+    rng = np.random.default_rng(9)
+    Q = rng.normal(size=(len(shifts), q.size)) + 1j * rng.normal(size=(len(shifts), q.size))
+    cfg, box, src, ob, prm = objects(fp, case, pos, q, obs)
+    sw = fp.build_sweep_plan(cfg, box, src, ob, prm, 0, shifts)
+    u_host = sw.evaluate(Q)
+    u_pin = torch.empty(u_host.shape, dtype=torch.complex128).pin_memory()
+    q_pin = torch.from_numpy(Q).pin_memory()
+    sw.evaluate(q_pin.numpy(), out=u_pin.numpy())
+    u_dev = sw.evaluate(torch.from_numpy(Q).cuda()).cpu().numpy()
+    assert np.array_equal(u_host, u_dev)
+    assert np.array_equal(u_host, u_pin.numpy())
+    assert np.array_equal(u_dev, sw.evaluate(torch.from_numpy(Q).cuda()).cpu().numpy())
+    with pytest.raises(ValueError):
+        sw.evaluate(Q[:3])
