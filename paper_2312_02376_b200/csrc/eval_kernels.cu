@@ -570,12 +570,15 @@ void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- K5a
-// Each warp scatters its contiguous chunk of points into a private copy of the
-// far source grid in shared memory (lanes own distinct taps of one point, so
-// no collisions); warps are summed in order, blocks in order by k_far_reduce.
-// Points are consumed in warp-sized batches whose stencil data is staged in
-// shared memory with one coalesced load per lane, so the per-point loop never
-// waits on global memory.
+// Each warp takes a contiguous chunk of the (cell-sorted) points; lane l owns
+// the stencil taps l, l + 32, ... and accumulates w * q in registers while the
+// far stencil start stays the same (consecutive sorted points share it for runs
+// of ~10 near cells), flushing the run into the warp's private copy of the far
+// source grid in shared memory when the start changes (lanes own distinct
+// taps, so no collisions; a warp barrier orders consecutive flushes).  Warps
+// are summed in order, blocks in order by k_far_reduce: fixed order throughout.
+// Point data is staged in shared memory in warp-sized batches with one
+// coalesced load per lane.
 template <int WF>
 __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
     extern __shared__ double smem_d[];
@@ -584,15 +587,44 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
     const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cplx* sgrid = reinterpret_cast<cplx*>(smem_d);
     constexpr int REC = 3 * WF + 2;                       // weights + q per staged point
+    constexpr int TPL = (WF * WF * WF + 31) / 32;         // taps per lane
     double* stage = smem_d + 2 * (size_t)nf * warps + warp * (32 * REC);
     int* sstart = reinterpret_cast<int*>(smem_d + 2 * (size_t)nf * warps + warps * 32 * REC) + warp * 96;
     for (int t = threadIdx.x; t < nf * warps; t += blockDim.x) sgrid[t] = mk(0.0);
     __syncthreads();
     cplx* mine = sgrid + warp * nf;
     const int wfx = a.fs.w[0], wfy = a.fs.w[1], wfz = a.fs.w[2];
+    // this lane's taps; taps beyond a single-plane axis are skipped (they would
+    // alias another lane's node)
+    int ta[TPL], tb[TPL], tc[TPL];
+    bool tok[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) {
+        const int tp = lane + 32 * t;
+        tc[t] = tp % WF;
+        tb[t] = (tp / WF) % WF;
+        ta[t] = tp / (WF * WF);
+        tok[t] = tp < WF * WF * WF && ta[t] < wfx && tb[t] < wfy && tc[t] < wfz;
+    }
+    double accr[TPL], acci[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) accr[t] = acci[t] = 0.0;
+    int c0 = -1, c1 = 0, c2 = 0;   // far stencil start of the open run
+    auto flush = [&]() {
+#pragma unroll
+        for (int t = 0; t < TPL; ++t) {
+            if (!tok[t]) continue;
+            cplx& d = mine[((c0 + ta[t]) * nfy + (c1 + tb[t])) * nfz + (c2 + tc[t])];
+            d.re += accr[t];
+            d.im += acci[t];
+            accr[t] = acci[t] = 0.0;
+        }
+        __syncwarp();
+    };
     const int64_t stride = (int64_t)gridDim.x * warps * 32;
     for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < a.far_n; base += stride) {
         const int64_t p = base + lane;
+        __syncwarp();
         if (p < a.far_n) {
             const double* w = a.src_fw + p * 3 * WF;
 #pragma unroll
@@ -609,21 +641,22 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
         for (int j = 0; j < cnt; ++j) {
             const double* r = stage + j * REC;
             const int s0 = sstart[3 * j], s1 = sstart[3 * j + 1], s2 = sstart[3 * j + 2];
-            const double qre = r[3 * WF], qim = r[3 * WF + 1];
-            // compile-time tap decomposition; taps beyond a single-plane axis are
-            // skipped (they would alias another lane's node)
-#pragma unroll
-            for (int tp = lane; tp < WF * WF * WF; tp += 32) {
-                const int ic = tp % WF, ib = (tp / WF) % WF, ia = tp / (WF * WF);
-                if (ia >= wfx || ib >= wfy || ic >= wfz) continue;
-                const double wgt = (r[ia] * r[WF + ib]) * r[2 * WF + ic];
-                const int node = ((s0 + ia) * nfy + (s1 + ib)) * nfz + (s2 + ic);
-                mine[node].re += wgt * qre;
-                mine[node].im += wgt * qim;
+            if (s0 != c0 || s1 != c1 || s2 != c2) {   // warp-uniform
+                if (c0 >= 0) flush();
+                c0 = s0;
+                c1 = s1;
+                c2 = s2;
             }
-            __syncwarp();
+            const double qre = r[3 * WF], qim = r[3 * WF + 1];
+#pragma unroll
+            for (int t = 0; t < TPL; ++t) {
+                const double wgt = (r[ta[t]] * r[WF + tb[t]]) * r[2 * WF + tc[t]];
+                accr[t] += wgt * qre;
+                acci[t] += wgt * qim;
+            }
         }
     }
+    if (c0 >= 0) flush();
     __syncthreads();
     for (int t = threadIdx.x; t < nf; t += blockDim.x) {
         cplx s = mk(0.0);

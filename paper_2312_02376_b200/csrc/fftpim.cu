@@ -1056,7 +1056,7 @@ void build(FftpimPlan* P) {
         }
         P->sw_omega = dalloc<cplx>(P, (int64_t)P->sw_E * NS);
         CK(cudaMemcpyAsync(P->sw_omega, omega.data(), sizeof(cplx) * omega.size(), cudaMemcpyHostToDevice, s));
-        P->sw_qt = dalloc<cplx>(P, N * P->sw_E);
+        P->sw_qt = dalloc<cplx>(P, 3 * N * P->sw_E);   // code-phased charges, c = -1, 0, 1
         P->sw_corr = dalloc<cplx>(P, Mown * P->sw_E);
         CK(cudaStreamSynchronize(s));
     }
@@ -1636,6 +1636,14 @@ int fftpim_sweep_create(const FftpimProblem* p, int32_t axis, int32_t n_exc, con
 // chain, K1, the FFT stages with the excitation's kernel_hat, the observer pass
 // without the K4 term -- memory/latency-bound) run on the high-priority stream;
 // after both join, one pass adds the K4 sums to every potential.
+// the batched K4 of a sweep: code-phased charge copies, then all excitations' sums
+static void sweep_k4(FftpimPlan* P, const double* q, cudaStream_t s) {
+    const int E = P->sw_E, NS = P->sw_ncomp + 2;
+    launch_sweep_permute((const cplx*)q, P->src_perm, P->N, E, P->sw_omega, NS, P->prob.i_d, P->sw_qt, s);
+    launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, P->N, E,
+                      P->sw_omega, P->sw_corr, P->M, s);
+}
+
 // `ready` (host entry): event e marks excitation e's charges resident; chain e
 // waits for it and the batched K4 for the last one.
 static void sweep_evaluate(FftpimPlan* P, const double* q, double* u, cudaStream_t s,
@@ -1649,9 +1657,7 @@ static void sweep_evaluate(FftpimPlan* P, const double* q, double* u, cudaStream
         CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
     }
     if (ready) CK(cudaStreamWaitEvent(sc, ready[E - 1], 0));
-    launch_sweep_permute((const cplx*)q, P->src_perm, P->N, E, P->sw_qt, sc);
-    launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, E, P->sw_omega,
-                      P->sw_corr, P->M, sc);
+    sweep_k4(P, q, sc);
     const int64_t nk = prod3(P->far_kdims);
     if (!P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, sn));
     for (int e = 0; e < E; ++e) {
@@ -1756,9 +1762,7 @@ int fftpim_sweep_profile(FftpimPlan* plan, const double* q, double* u, void* str
         for (auto& e : ev) CK(cudaEventCreate(&e));
         FftpimPlan* P = plan;
         CK(cudaEventRecord(ev[0], s));
-        launch_sweep_permute((const cplx*)q, P->src_perm, P->N, P->sw_E, P->sw_qt, s);
-        launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, P->sw_E,
-                          P->sw_omega, P->sw_corr, P->M, s);
+        sweep_k4(P, q, s);
         CK(cudaEventRecord(ev[1], s));
         sweep_evaluate(P, q, u, s);
         CK(cudaEventRecord(ev[2], s));

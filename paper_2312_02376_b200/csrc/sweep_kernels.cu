@@ -8,9 +8,10 @@
 // folded in) and
 //     coef_e = sum_j exp(-j (c_a + j - i_d) k_e L_a) B_j.
 // The batched K4 below streams the components once for all E excitations: a
-// warp per observer, lanes own excitations, per-power accumulators
-// S_m = sum_pairs B_j q_e[src] (m = c_a + j - i_d), and at the row end
-// corr_e = sum_m omega_e^m S_m.  Fixed order, no atomics.
+// warp per observer, lanes own excitations, per-component accumulators
+// S_j = sum_pairs B_j omega_e^(c_a) q_e[src] (the code phase is pre-applied to
+// three copies of the charges), and at the row end
+// corr_e = sum_j omega_e^(j - i_d) S_j.  Fixed order, no atomics.
 #include <cstdlib>
 
 #include "geom.cuh"
@@ -35,47 +36,93 @@ void launch_sweep_pack_src(int* pair_src, const unsigned char* codeid, const sig
     fftpim_count_launch();
 }
 
-// qt[i][e] = q[e][perm[i]]  (sorted order, excitation fastest)
+// Code-phased charges: qt3[c + 1][i][e] = omega_e^c q[e][perm[i]], c = -1, 0, 1
+// (sorted order, excitation fastest), omega_e^m = exp(-j m k_e L_a).  The code
+// phase of a pair then rides on the charge row it reads, so the batched K4
+// keeps one accumulator per component and never branches on the code.
 __global__ void k_sweep_permute(const cplx* __restrict__ q, const int* __restrict__ perm, int64_t N, int E,
-                                cplx* __restrict__ qt) {
+                                const cplx* __restrict__ omega, int NS, int h, cplx* __restrict__ qt3) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= N * E) return;
     const int64_t i = t / E;
     const int e = (int)(t - i * E);
-    qt[t] = q[(int64_t)e * N + perm[i]];
+    const cplx v = q[(int64_t)e * N + perm[i]];
+    qt3[t] = omega[e * NS + h] * v;           // m = -1
+    qt3[N * E + t] = v;                       // m = 0
+    qt3[2 * N * E + t] = omega[e * NS + h + 2] * v;   // m = +1
 }
 
-void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, cplx* qt, cudaStream_t s) {
+void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, const cplx* omega, int NS, int h,
+                          cplx* qt3, cudaStream_t s) {
     if (N == 0) return;
-    k_sweep_permute<<<nblk(N * E, 256), 256, 0, s>>>(q, perm, N, E, qt);
+    k_sweep_permute<<<nblk(N * E, 256), 256, 0, s>>>(q, perm, N, E, omega, NS, h, qt3);
     fftpim_count_launch();
 }
 
-// warp per sorted observer; lane l owns excitations l and l + 32 (E <= 64).
+// Warp per sorted observer; lane l owns excitations l and l + 32 (E <= 64).
 // Pairs are taken 32 at a time: lane k stages pair k's packed source and
 // components in shared memory (coalesced loads), then the warp walks the 32
-// pairs reading them as broadcasts, four pairs' q rows in flight at a time.
+// pairs reading them as broadcasts, SWEEP_U pairs' charge rows in flight at a
+// time.  S_j += B_j qt3[c][src]; at the row end corr_e = sum_j omega_e^(j - h) S_j.
 #ifndef SWEEP_U   // pairs whose q rows are in flight together
 #define SWEEP_U 2
 #endif
-template <int NC, bool TWO, bool HALVES>
-__global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ ptr, const int* __restrict__ psrc,
-                                                    const cplx* __restrict__ comp, int64_t P,
-                                                    const cplx* __restrict__ qt, int E,
-                                                    const cplx* __restrict__ omega, cplx* __restrict__ corr,
-                                                    int64_t M) {
-    constexpr int NS = NC + 2;   // powers m = -(h+1) .. h+1, h = NC / 2
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 3
+#endif
+template <int NC, bool TWO, bool FULL, bool TAIL>
+__device__ __forceinline__ void sweep_pairs(const int* sv, const cplx (*sb)[32], int cnt, const cplx* __restrict__ qt3,
+                                            int64_t NE, int E, int e0, int e1, bool ok0, bool ok1, double* s0r,
+                                            double* s0i, double* s1r, double* s1i) {
+    const int kend = TAIL ? cnt : 32;
+    for (int k0 = 0; k0 < kend; k0 += SWEEP_U) {
+        cplx q0[SWEEP_U], q1[SWEEP_U];
+#pragma unroll
+        for (int u = 0; u < SWEEP_U; ++u) {
+            const bool in = !TAIL || k0 + u < cnt;
+            const int v = in ? sv[k0 + u] : 0;
+            const cplx* qrow = qt3 + (int64_t)((unsigned)v >> 30) * NE + (int64_t)(v & 0x3fffffff) * E;
+            q0[u] = (in && (FULL || ok0)) ? qrow[e0] : mk(0.0);
+            if (TWO) q1[u] = (in && (FULL || ok1)) ? qrow[e1] : mk(0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < SWEEP_U; ++u) {
+            const int k = TAIL ? min(k0 + u, 31) : k0 + u;   // tail: padded pairs carry q = 0
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                const cplx b = sb[j][k];
+                s0r[j] = fma(b.re, q0[u].re, s0r[j]);
+                s0r[j] = fma(-b.im, q0[u].im, s0r[j]);
+                s0i[j] = fma(b.re, q0[u].im, s0i[j]);
+                s0i[j] = fma(b.im, q0[u].re, s0i[j]);
+                if (TWO) {
+                    s1r[j] = fma(b.re, q1[u].re, s1r[j]);
+                    s1r[j] = fma(-b.im, q1[u].im, s1r[j]);
+                    s1i[j] = fma(b.re, q1[u].im, s1i[j]);
+                    s1i[j] = fma(b.im, q1[u].re, s1i[j]);
+                }
+            }
+        }
+    }
+}
+
+template <int NC, bool TWO, bool FULL>
+__global__ void __launch_bounds__(256, SWEEP_MINB)
+    k_corr_sweep(const int64_t* __restrict__ ptr, const int* __restrict__ psrc, const cplx* __restrict__ comp,
+                 int64_t P, const cplx* __restrict__ qt3, int64_t N, int E, const cplx* __restrict__ omega,
+                 cplx* __restrict__ corr, int64_t M) {
+    constexpr int h = NC / 2, NS = NC + 2;
     __shared__ cplx s_b[8][NC][32];
     __shared__ int s_v[8][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t i = HALVES ? gw >> 1 : gw;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (i >= M) return;
-    const int e0 = HALVES ? lane + 32 * (int)(gw & 1) : lane, e1 = lane + 32;
+    const int e0 = lane, e1 = lane + 32;
     const bool ok0 = e0 < E, ok1 = TWO && e1 < E;
-    double s0r[NS], s0i[NS], s1r[NS], s1i[NS];
+    const int64_t NE = N * E;
+    double s0r[NC], s0i[NC], s1r[NC], s1i[NC];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) s0r[k] = s0i[k] = s1r[k] = s1i[k] = 0.0;
+    for (int k = 0; k < NC; ++k) s0r[k] = s0i[k] = s1r[k] = s1i[k] = 0.0;
     const int64_t p0 = ptr[i], p1 = ptr[i + 1];
     for (int64_t b = p0; b < p1; b += 32) {
         const int cnt = (int)min((int64_t)32, p1 - b);
@@ -84,59 +131,33 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
             s_v[wid][lane] = psrc[b + lane];
 #pragma unroll
             for (int j = 0; j < NC; ++j) s_b[wid][j][lane] = comp[(int64_t)j * P + b + lane];
+        } else {
+            s_v[wid][lane] = 0;
+#pragma unroll
+            for (int j = 0; j < NC; ++j) s_b[wid][j][lane] = mk(0.0);
         }
         __syncwarp();
-        for (int k0 = 0; k0 < cnt; k0 += SWEEP_U) {
-            int v[SWEEP_U];
-            cplx q0[SWEEP_U], q1[SWEEP_U];
-#pragma unroll
-            for (int u = 0; u < SWEEP_U; ++u) {
-                const bool in = k0 + u < cnt;
-                v[u] = in ? s_v[wid][k0 + u] : 0;
-                const cplx* qrow = qt + (int64_t)(v[u] & 0x3fffffff) * E;
-                q0[u] = (in && ok0) ? qrow[e0] : mk(0.0);
-                q1[u] = (in && ok1) ? qrow[e1] : mk(0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < SWEEP_U; ++u) {
-                if (k0 + u >= cnt) break;
-                const int ca = (v[u] >> 30) & 3;   // code along the axis + 1 (warp-uniform)
-                cplx bj[NC];
-#pragma unroll
-                for (int j = 0; j < NC; ++j) bj[j] = s_b[wid][j][k0 + u];
-                // S[ca + j] += B_j q
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    if (ca != c) continue;
-#pragma unroll
-                    for (int j = 0; j < NC; ++j) {
-                        s0r[c + j] += bj[j].re * q0[u].re - bj[j].im * q0[u].im;
-                        s0i[c + j] += bj[j].re * q0[u].im + bj[j].im * q0[u].re;
-                        if (TWO) {
-                            s1r[c + j] += bj[j].re * q1[u].re - bj[j].im * q1[u].im;
-                            s1i[c + j] += bj[j].re * q1[u].im + bj[j].im * q1[u].re;
-                        }
-                    }
-                }
-            }
-        }
+        if (cnt == 32)
+            sweep_pairs<NC, TWO, FULL, false>(s_v[wid], s_b[wid], cnt, qt3, NE, E, e0, e1, ok0, ok1, s0r, s0i, s1r, s1i);
+        else
+            sweep_pairs<NC, TWO, FULL, true>(s_v[wid], s_b[wid], cnt, qt3, NE, E, e0, e1, ok0, ok1, s0r, s0i, s1r, s1i);
     }
-    // corr_e = sum_m omega_e^m S_m
-    if (ok0) {
+    // corr_e = sum_j omega_e^(j - h) S_j   (table index m + h + 1)
+    if (FULL || ok0) {
         double r = 0.0, im = 0.0;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const cplx w = omega[(int64_t)e0 * NS + k];
+        for (int k = 0; k < NC; ++k) {
+            const cplx w = omega[(int64_t)e0 * NS + k + 1];
             r += w.re * s0r[k] - w.im * s0i[k];
             im += w.re * s0i[k] + w.im * s0r[k];
         }
         corr[i * E + e0] = cplx{r, im};
     }
-    if (ok1) {
+    if (TWO && (FULL || ok1)) {
         double r = 0.0, im = 0.0;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const cplx w = omega[(int64_t)e1 * NS + k];
+        for (int k = 0; k < NC; ++k) {
+            const cplx w = omega[(int64_t)e1 * NS + k + 1];
             r += w.re * s1r[k] - w.im * s1i[k];
             im += w.re * s1i[k] + w.im * s1r[k];
         }
@@ -145,29 +166,18 @@ __global__ void __launch_bounds__(256) k_corr_sweep(const int64_t* __restrict__ 
 }
 
 void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp, int ncomp, int64_t P,
-                       const cplx* qt, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s) {
+                       const cplx* qt3, int64_t N, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s) {
     if (M == 0) return;
-    // E > 32: two warps per observer (one per 32 excitations, adjacent in the
-    // block so the second reads the pair data from L1) or one warp with two
-    // excitations per lane (default; measured faster, FFTPIM_SWEEP_HALVES=1 for the other)
-    static const bool halves = [] {
-        const char* e = getenv("FFTPIM_SWEEP_HALVES");
-        return e && e[0] == '1';
-    }();
-    const bool two = E > 32;
-    if (two && halves) {
-        const int blocks = nblk(M * 64, 256);
-        if (ncomp == 3)
-            k_corr_sweep<3, false, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
-        else
-            k_corr_sweep<5, false, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
-        fftpim_count_launch();
-        return;
-    }
     const int blocks = nblk(M * 32, 256);
-#define KS(NC)                                                                                              \
-    if (two) k_corr_sweep<NC, true, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M); \
-    else k_corr_sweep<NC, false, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt, E, omega, corr, M);
+#define KS(NC)                                                                                                   \
+    if (E == 64)                                                                                                 \
+        k_corr_sweep<NC, true, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M); \
+    else if (E > 32)                                                                                             \
+        k_corr_sweep<NC, true, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M); \
+    else if (E == 32)                                                                                            \
+        k_corr_sweep<NC, false, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M); \
+    else                                                                                                         \
+        k_corr_sweep<NC, false, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M);
     if (ncomp == 3) {
         KS(3)
     } else {
