@@ -138,6 +138,31 @@ FFTPIM_API int fftpim_sweep_profile(FftpimPlan* plan, const double* q, double* u
 /* axis and excitation count of a sweep plan (-1, 0 for ordinary plans). */
 FFTPIM_API int fftpim_sweep_info(const FftpimPlan* plan, int32_t* axis, int32_t* n_exc);
 
+/* Brute-force direct sums: the reference's accuracy oracle (oracle.py:62-123,
+ * SURVEY.md 8f rank 4), one converged periodic-Green's-function series per
+ * (observer, source) pair on the device.
+ *   mode 0: eval_direct           u_m = sum_n G_p(r_m - r_n) q_n      (oracle.py:92-97)
+ *   mode 1: eval_direct_farzone   G_p minus the |i| <= p->i_d images   (oracle.py:100-111)
+ *   mode 2: eval_free_space       sum_n exp(-j k0 r) / (4 pi r) q_n   (oracle.py:114-123)
+ * Uses p->dim, regime, L, k0, kshift, i_d (mode 1), n_src, n_obs, src_pos,
+ * obs_pos (HOST, NULL = sources), device.  tol / max_terms / consecutive_small
+ * are the TruncationPolicy (pgf.py:40-58).  q (n_src) and u (n_obs) are HOST
+ * complex128.  Observers are taken in chunks of 64 like the reference: a chunk
+ * with a pair violating the separation rule (oracle.py:35-59) keeps u = 0 and
+ * reports its separation failures, otherwise its non-converged pairs are
+ * reported.  failures: optional (max_failures, 3) int64 records
+ * (observer, source, 1 = separation | 2 = not converged) in the reference's
+ * order; rep->n_failures counts all of them.  Mode 2 returns FFTPIM_DOMAIN
+ * when an observer coincides with a source (the reference's ZeroDivisionError). */
+typedef struct FftpimDirectReport {
+    int64_t worst_terms;        /* longest series over the evaluated chunks */
+    int64_t n_failures;
+    int64_t n_skipped_chunks;   /* chunks left at 0 by separation failures */
+} FftpimDirectReport;
+FFTPIM_API int fftpim_direct_evaluate(const FftpimProblem* p, int32_t mode, double tol, int64_t max_terms,
+                                      int32_t consecutive_small, const double* q, double* u, int64_t* failures,
+                                      int64_t max_failures, FftpimDirectReport* rep);
+
 /* Same with HOST q/u (pinned or pageable): H2D copy, evaluate, D2H copy,
  * synchronous.  This is the call the reference's FFI binding makes. */
 FFTPIM_API int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch,

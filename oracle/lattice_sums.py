@@ -69,9 +69,10 @@ def image_sum(points, pb: Problem, h, drop=False, tol=None):
     return acc
 
 
-def drive(points, tol, lead, layer, first):
-    """pgf.py:166-195: every point keeps adding layers until CONSECUTIVE_SMALL layers
-    in a row satisfy |layer| <= tol*max(|total|, 1e-300)."""
+def drive(points, tol, lead, layer, first, max_terms=MAX_TERMS, consecutive=CONSECUTIVE_SMALL):
+    """pgf.py:166-195: every point keeps adding layers until `consecutive` layers
+    in a row satisfy |layer| <= tol*max(|total|, 1e-300), or max_terms is reached
+    (TruncationPolicy, pgf.py:40-58)."""
     n = points.shape[0]
     total = np.zeros(n, dtype=complex)
     terms = np.zeros(n, dtype=np.int64)
@@ -88,9 +89,9 @@ def drive(points, tol, lead, layer, first):
         terms[live] += c
         small = np.abs(v) <= tol * np.maximum(np.abs(total[live]), 1e-300)
         quiet[live] = np.where(small, quiet[live] + 1, 0)
-        fin = quiet[live] >= CONSECUTIVE_SMALL
+        fin = quiet[live] >= consecutive
         done[live[fin]] = True
-        live = live[~fin & (terms[live] < MAX_TERMS)]
+        live = live[~fin & (terms[live] < max_terms)]
         s += 1
     return total, terms, done
 
@@ -106,7 +107,7 @@ def shell(s: int):
     return ms, ns
 
 
-def spectral(points, pb: Problem, tol):
+def spectral(points, pb: Problem, tol, **policy):
     """Floquet series; pgf.py:215-295."""
     if pb.regime == Regime.NPSP:
         raise SeriesError("domain", "spectral series diverges for NPSP")
@@ -137,7 +138,7 @@ def spectral(points, pb: Problem, tol):
                 acc += np.exp(-1j * km * p[:, 0]) * h0(kr * rho) / (4j * lx)
             return acc, len(ms)
 
-        return drive(pts, tol, None, layer1, 0)
+        return drive(pts, tol, None, layer1, 0, **policy)
 
     three = pb.dim == 3
 
@@ -169,7 +170,7 @@ def spectral(points, pb: Problem, tol):
                 acc += (np.exp(-1j * (a * x + b * y)) * f / (2j * c * lx * ly)).sum(axis=0)
         return acc, kxs.size
 
-    return drive(pts, tol, None, layer23, 0)
+    return drive(pts, tol, None, layer23, 0, **policy)
 
 
 def _log_trig(y, a, ly):
@@ -182,7 +183,7 @@ def _log_trig(y, a, ly):
     return np.log(arg)
 
 
-def lattice(points, pb: Problem, tol):
+def lattice(points, pb: Problem, tol, **policy):
     """NPSP lattice series; pgf.py:328-425.  Note the 3D lead's z-image range and
     the layers' (n, k) ranges come from the extrema over the *whole* call."""
     if pb.regime != Regime.NPSP:
@@ -210,7 +211,7 @@ def lattice(points, pb: Problem, tol):
                 v[ok] = k0(arg[ok])
             return modulate(v, p, m), 1
 
-        return drive(pts, tol, lead1, layer1, 1)
+        return drive(pts, tol, lead1, layer1, 1, **policy)
 
     if pb.dim == 2:
         def lead2(p):
@@ -233,7 +234,7 @@ def lattice(points, pb: Problem, tol):
                     cnt[ok] += 1
             return modulate(acc, p, m), np.maximum(cnt, 1)
 
-        return drive(pts, tol, lead2, layer2, 1)
+        return drive(pts, tol, lead2, layer2, 1, **policy)
 
     def lead3(p):
         y, z = p[:, 1], p[:, 2]
@@ -263,7 +264,7 @@ def lattice(points, pb: Problem, tol):
                     cnt[ok] += 1
         return modulate(acc, p, m), np.maximum(cnt, 1)
 
-    return drive(pts, tol, lead3, layer3, 1)
+    return drive(pts, tol, lead3, layer3, 1, **policy)
 
 
 def far_kernel(points, pb: Problem):

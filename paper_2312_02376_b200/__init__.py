@@ -11,6 +11,7 @@ from .api import (FarZonePlan, NativePlan, NearZonePlan, SolvePlan, SolveResult,
                   save_far_kernel, solve)
 from .exceptions import (DomainError, KernelCacheError, NativeLibraryError, NotConvergedError,
                          PerisumError, SeparationError, ValidationError, WoodAnomalyError)
+from .direct import OracleReport, TruncationPolicy, eval_direct, eval_direct_farzone, eval_free_space
 from .sweep import SweepPlan, build_sweep_plan
 from .problem import (ObserverPointSet, Periodicity, PeriodicityConfig, PotentialField, Regime,
                       SolverParams, SourcePointSet, TargetBox, ValidationReport, auto_near_dims,
@@ -25,5 +26,6 @@ __all__ = [
     "NotConvergedError", "PerisumError", "SeparationError", "ValidationError", "WoodAnomalyError",
     "ObserverPointSet", "Periodicity", "PeriodicityConfig", "PotentialField", "Regime",
     "SolverParams", "SourcePointSet", "TargetBox", "ValidationReport", "auto_near_dims",
-    "validate_problem", "SweepPlan", "build_sweep_plan",
+    "validate_problem", "SweepPlan", "build_sweep_plan", "OracleReport", "TruncationPolicy", "eval_direct",
+    "eval_direct_farzone", "eval_free_space",
 ]

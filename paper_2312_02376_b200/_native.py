@@ -47,12 +47,16 @@ class Info(C.Structure):
     ]
 
 
+class DirectReport(C.Structure):
+    _fields_ = [("worst_terms", C.c_int64), ("n_failures", C.c_int64), ("n_skipped_chunks", C.c_int64)]
+
+
 EXPORTED = ("fftpim_plan_create", "fftpim_plan_evaluate", "fftpim_plan_evaluate_host",
             "fftpim_plan_info", "fftpim_plan_export", "fftpim_plan_set_far_kernel",
             "fftpim_plan_destroy", "fftpim_last_error", "fftpim_launch_count", "fftpim_plan_profile",
             "fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
             "fftpim_group_destroy", "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info",
-            "fftpim_sweep_profile", "fftpim_sweep_evaluate_host")
+            "fftpim_sweep_profile", "fftpim_sweep_evaluate_host", "fftpim_direct_evaluate")
 N_STAGES = 9
 STAGES = ("permute_q", "far_project", "far_sum", "near_project", "fft_forward", "spectrum_mul",
           "fft_inverse", "corr_matvec", "observers")
@@ -95,9 +99,11 @@ def load(path: str = LIB_PATH):
     lib.fftpim_sweep_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     lib.fftpim_sweep_profile.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_double)]
     lib.fftpim_sweep_evaluate_host.argtypes = [vp, vp, vp]
+    lib.fftpim_direct_evaluate.argtypes = [C.POINTER(Problem), C.c_int32, C.c_double, C.c_int64, C.c_int32,
+                                           vp, vp, vp, C.c_int64, C.POINTER(DirectReport)]
     for name in ("fftpim_nccl_unique_id", "fftpim_group_create", "fftpim_group_evaluate", "fftpim_group_info",
                  "fftpim_sweep_create", "fftpim_sweep_evaluate", "fftpim_sweep_info", "fftpim_sweep_profile",
-                 "fftpim_sweep_evaluate_host"):
+                 "fftpim_sweep_evaluate_host", "fftpim_direct_evaluate"):
         getattr(lib, name).restype = C.c_int
     lib.fftpim_last_error.restype = C.c_char_p
     lib.fftpim_launch_count.restype = C.c_int64

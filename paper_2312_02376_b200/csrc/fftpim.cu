@@ -165,6 +165,9 @@ void check_status(FftpimPlan* P, const char* phase) {
             case 47: detail = "far kernel series did not converge at difference point " + std::to_string(st.a) +
                               " (terms used: " + std::to_string(st.b) + ")"; break;
             case 48: detail = "far kernel: image point coincides with evaluation point"; break;
+            case 60: detail = "observer " + std::to_string(st.a) + " coincides with source " + std::to_string(st.b); break;
+            case 61: detail = "image point coincides with evaluation point (observer " + std::to_string(st.a) +
+                              ", source " + std::to_string(st.b) + ")"; break;
             default: detail = "code " + std::to_string(st.where);
         }
         snprintf(buf, sizeof(buf), "%s during %s: ", what, phase);
@@ -487,6 +490,7 @@ static int64_t tabulate_far(FftpimPlan* P, const double ks[3][2], const ImageSet
     fp.zmax = zmax;
     fp.max_terms = 1000000;
     fp.max_layers = 200000;
+    fp.consecutive = 3;
     static const GLTable gl = gauss_laguerre_half();
     launch_far_series(d_axes, P->far_kdims, fp, im, gl, out, P->status, s);
     check_status(P, "far kernel tabulation");
@@ -1786,6 +1790,168 @@ int fftpim_sweep_info(const FftpimPlan* plan, int32_t* axis, int32_t* n_exc) {
     *axis = plan->sweep ? plan->sw_axis : -1;
     *n_exc = plan->sweep ? plan->sw_E : 0;
     return FFTPIM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Brute-force direct sums (oracle.py:62-123) -- see direct_kernels.cu.
+int fftpim_direct_evaluate(const FftpimProblem* p, int32_t mode, double tol, int64_t max_terms,
+                           int32_t consecutive_small, const double* q, double* u, int64_t* failures,
+                           int64_t max_failures, FftpimDirectReport* rep) {
+    if (!p || !q || !u || !rep || !p->src_pos) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (mode < 0 || mode > 2) return fail(Fail{FFTPIM_VALUE, "mode must be 0 (direct), 1 (far zone) or 2 (free space)"});
+    if (mode != 2 && (p->dim < 1 || p->dim > 3)) return fail(Fail{FFTPIM_VALUE, "dim must be 1, 2 or 3"});
+    if (mode != 2 && !(tol > 0.0)) return fail(Fail{FFTPIM_VALUE, "tol must be positive"});
+    if (mode != 2 && (max_terms < 1 || consecutive_small < 1))
+        return fail(Fail{FFTPIM_VALUE, "max_terms and consecutive_small must be >= 1"});
+    if (mode == 1 && (p->i_d < 0 || p->i_d > 2)) return fail(Fail{FFTPIM_VALUE, "i_d must be in [0, 2]"});
+    memset(rep, 0, sizeof(*rep));
+    const int64_t N = p->n_src, M = p->n_obs;
+    if (M <= 0) return FFTPIM_OK;
+    FftpimPlan* P = new FftpimPlan();   // scratch owner of the device buffers
+    try {
+        P->device = p->device;
+        P->prob = *p;
+        CK(cudaSetDevice(P->device));
+        CK(cudaStreamCreateWithFlags(&P->build_stream, cudaStreamNonBlocking));
+        cudaStream_t s = P->build_stream;
+        P->status = dalloc<DevStatus>(P, 1);
+        CK(cudaMemsetAsync(P->status, 0, sizeof(DevStatus), s));
+        const double* obs_h = p->obs_pos ? p->obs_pos : p->src_pos;
+        double* d_src = dalloc<double>(P, 3 * std::max<int64_t>(N, 1));
+        double* d_obs = dalloc<double>(P, 3 * M);
+        cplx* d_q = dalloc<cplx>(P, std::max<int64_t>(N, 1));
+        cplx* d_u = dalloc<cplx>(P, M);
+        if (N > 0) {
+            CK(cudaMemcpyAsync(d_src, p->src_pos, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(d_q, q, sizeof(cplx) * N, cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaMemcpyAsync(d_obs, obs_h, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
+        if (N == 0) {
+            CK(cudaMemsetAsync(d_u, 0, sizeof(cplx) * M, s));
+        } else {
+            const int64_t CH = 64;   // oracle.py:20
+            const int64_t nchunk = (M + CH - 1) / CH;
+            // z extrema of each chunk's differences (pgf.py:394-397): max/min of
+            // fl(o - s) are fl(max o - min s), fl(min o - max s) (rounding is monotone)
+            double szmin = 1e300, szmax = -1e300;
+            for (int64_t j = 0; j < N; ++j) {
+                szmin = std::min(szmin, p->src_pos[3 * j + 2]);
+                szmax = std::max(szmax, p->src_pos[3 * j + 2]);
+            }
+            std::vector<double> zr(2 * nchunk);
+            for (int64_t c = 0; c < nchunk; ++c) {
+                double omin = 1e300, omax = -1e300;
+                for (int64_t i = c * CH; i < std::min(M, (c + 1) * CH); ++i) {
+                    omin = std::min(omin, obs_h[3 * i + 2]);
+                    omax = std::max(omax, obs_h[3 * i + 2]);
+                }
+                zr[2 * c] = omin - szmax;
+                zr[2 * c + 1] = omax - szmin;
+            }
+            double* d_zr = dalloc<double>(P, 2 * nchunk);
+            CK(cudaMemcpyAsync(d_zr, zr.data(), sizeof(double) * zr.size(), cudaMemcpyHostToDevice, s));
+            int* d_sep = dalloc<int>(P, nchunk);
+            long long* d_terms = dalloc<long long>(P, nchunk);
+            CK(cudaMemsetAsync(d_sep, 0, sizeof(int) * nchunk, s));
+            CK(cudaMemsetAsync(d_terms, 0, sizeof(long long) * nchunk, s));
+            // rows per launch: whole chunks, at most ~32 M pairs of scratch
+            const int64_t cap = (int64_t)1 << 25;
+            int64_t rows = std::max<int64_t>(CH, (cap / N) / CH * CH);
+            rows = std::min(rows, nchunk * CH);
+            cplx* d_vals = dalloc<cplx>(P, rows * N);
+            unsigned char* d_flags = dalloc<unsigned char>(P, rows * N);
+            double maxLp = 0.0;
+            for (int a = 0; a < std::max(1, std::min(3, p->dim)); ++a) maxLp = std::max(maxLp, p->L[a]);
+            FarSeriesParams fp{};
+            fp.dim = p->dim;
+            fp.npsp = p->regime == FFTPIM_NPSP;
+            for (int a = 0; a < 3; ++a) {
+                fp.L[a] = p->L[a];
+                fp.ks_re[a] = p->kshift[a][0];
+                fp.ks_im[a] = p->kshift[a][1];
+            }
+            fp.k0_re = p->k0[0];
+            fp.k0_im = p->k0[1];
+            if (mode != 2) {
+                fp.tol = tol;
+                fp.cutoff = std::log(1.0 / tol) + 8.0;   // TruncationPolicy.inner_cutoff
+                fp.sep = 1e-13 * std::max(maxLp, 1.0);   // pgf.py:93-94
+                fp.wood = 1e-8 * 2.0 * M_PI / maxLp;     // pgf.py:88-90
+                fp.max_terms = max_terms;
+                fp.max_layers = 200000;
+                fp.consecutive = consecutive_small;
+            }
+            ImageSet im{};
+            im.k0_re = p->k0[0];
+            im.k0_im = p->k0[1];
+            im.sep_tol = 1e-13 * std::max(maxLp, 1.0);
+            if (mode == 1) {
+                FftpimProblem pi = *p;
+                make_images(pi, p->kshift, im);
+            }
+            static const GLTable gl = gauss_laguerre_half();
+            DirectArgs a{};
+            a.src = d_src;
+            a.obs = d_obs;
+            a.q = d_q;
+            a.N = N;
+            a.zr = d_zr;
+            a.dim = p->dim;
+            a.npsp = fp.npsp;
+            a.far_only = mode == 1;
+            a.free_space = mode == 2;
+            for (int k = 0; k < 3; ++k) a.L[k] = p->L[k];
+            a.floor_t = 1e-12 * maxLp;   // oracle.py:31-32
+            a.vals = d_vals;
+            a.flags = d_flags;
+            a.chunk_sep = d_sep;
+            a.chunk_terms = d_terms;
+            std::vector<int> sep(nchunk);
+            std::vector<long long> terms(nchunk);
+            std::vector<unsigned char> flags;
+            int64_t nfail = 0;
+            for (int64_t m0 = 0; m0 < M; m0 += rows) {
+                a.m0 = m0;
+                a.mc = std::min(rows, M - m0);
+                launch_direct(a, fp, im, gl, d_u, P->status, s);
+                check_status(P, mode == 2 ? "free-space sum" : "direct periodic sum");
+                // failures in the reference's order: chunk by chunk, (observer, source)
+                // row-major; a chunk with separation failures reports only those
+                const int64_t c0 = m0 / CH, c1 = (m0 + a.mc + CH - 1) / CH;
+                CK(cudaMemcpy(sep.data() + c0, d_sep + c0, sizeof(int) * (c1 - c0), cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(terms.data() + c0, d_terms + c0, sizeof(long long) * (c1 - c0), cudaMemcpyDeviceToHost));
+                if (mode == 2) continue;
+                flags.resize((size_t)(a.mc * N));
+                CK(cudaMemcpy(flags.data(), d_flags, flags.size(), cudaMemcpyDeviceToHost));
+                for (int64_t c = c0; c < c1; ++c) {
+                    const unsigned char want = sep[c] ? 1 : 2;
+                    if (sep[c]) ++rep->n_skipped_chunks;
+                    else rep->worst_terms = std::max<int64_t>(rep->worst_terms, terms[c]);
+                    for (int64_t i = c * CH; i < std::min(M, (c + 1) * CH); ++i) {
+                        const unsigned char* fr = flags.data() + (i - m0) * N;
+                        for (int64_t j = 0; j < N; ++j) {
+                            if (fr[j] != want) continue;
+                            if (failures && nfail < max_failures) {
+                                failures[3 * nfail] = i;
+                                failures[3 * nfail + 1] = j;
+                                failures[3 * nfail + 2] = want;
+                            }
+                            ++nfail;
+                        }
+                    }
+                }
+            }
+            rep->n_failures = nfail;
+        }
+        CK(cudaMemcpyAsync(u, d_u, sizeof(cplx) * M, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fftpim_plan_destroy(P);
+        return FFTPIM_OK;
+    } catch (const Fail& f) {
+        if (P->build_stream) cudaStreamSynchronize(P->build_stream);
+        fftpim_plan_destroy(P);
+        return fail(f);
+    }
 }
 
 int fftpim_nccl_unique_id(void* out, int64_t bytes) {

@@ -16,6 +16,7 @@ struct FarSeriesParams {
     double zmin, zmax; // extrema over the whole point set (3D lattice lead, pgf.py:394-397)
     long long max_terms;
     int max_layers;
+    int consecutive;   // layers in a row below tol that stop a point (TruncationPolicy.consecutive_small)
 };
 
 // ---- plan build (build_kernels.cu) ----
@@ -74,6 +75,24 @@ void launch_code_tables(const CodeTables& tabs, int ncodes, const PairGeom& pg, 
                         cplx* tables, int64_t total, cudaStream_t s);
 void launch_far_series(const double* axes, const int kd[3], const FarSeriesParams& fp, const ImageSet& im,
                        const GLTable& gl, cplx* out, DevStatus* st, cudaStream_t s);
+
+// ---- brute-force direct sums (direct_kernels.cu) ----
+struct DirectArgs {
+    const double* src;          // (N, 3) device
+    const double* obs;          // (M, 3) device
+    const cplx* q;              // (N,)
+    int64_t N, m0, mc;          // this launch: observers [m0, m0 + mc), mc a multiple of 64 (or the tail)
+    const double* zr;           // per 64-observer chunk: z extrema of its differences (3D lattice lead)
+    int dim, npsp, far_only, free_space;
+    double L[3];
+    double floor_t;             // 1e-12 * max periodic L (oracle.py:31-32)
+    cplx* vals;                 // (mc, N) G q per pair
+    unsigned char* flags;       // (mc, N): 0 ok, 1 separation, 2 not converged
+    int* chunk_sep;             // per chunk: separation failures
+    long long* chunk_terms;     // per chunk: longest series
+};
+void launch_direct(const DirectArgs& a, const FarSeriesParams& fp, const ImageSet& im, const GLTable& gl,
+                   cplx* u, DevStatus* st, cudaStream_t s);
 
 // ---- evaluation (eval_kernels.cu) ----
 struct EvalArgs {
