@@ -335,8 +335,18 @@ def solve(cfg, box, src, obs, params=None, provider=None, kernel_cache=None) -> 
 
 
 def build_near_plan(cfg, box, src, obs, params, provider=None) -> NearZonePlan:
-    """nearzone.py:194-197 signature; validation follows the facade's rules."""
-    return NearZonePlan(_validated_native(cfg, box, src, obs, params))
+    """nearzone.py:194-197 signature; validation follows the facade's rules.
+    i_d = 0 builds a near-zone-only plan (free-space near kernel, no wrapped
+    copies, nearzone.py:205-212, :314), as the reference's bench baseline does
+    (cli.py:343-347); the far-zone and D_ER rules only apply for i_d >= 1."""
+    params = params or SolverParams()
+    if params.i_d != 0:
+        return NearZonePlan(_validated_native(cfg, box, src, obs, params))
+    report = validate_problem(cfg, box, src, obs, params)
+    rest = tuple(m for m in report.messages if "i_d must be" not in m and "error-correction range" not in m)
+    if rest:
+        raise ValidationError(type(report)(rest))
+    return NearZonePlan(NativePlan(cfg, box, src, obs, params))
 
 
 def eval_near(plan: NearZonePlan, q, provider=None):

@@ -508,7 +508,11 @@ void build(FftpimPlan* P) {
     P->M = M;
     P->npsp = pr.regime == FFTPIM_NPSP;
     if (N <= 0 || M <= 0) throw Fail{FFTPIM_VALUE, "empty source or observer set"};
-    if (pr.i_d < 1) throw Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"};
+    // i_d = 0: near zone only (free-space near kernel, no wrapped copies;
+    // nearzone.py:205-212, :314) -- the far engine needs i_d >= 1 (farzone.py:84-85)
+    if (pr.i_d < 0) throw Fail{FFTPIM_VALUE, "i_d must be >= 0"};
+    P->near_only = pr.i_d == 0;
+    if (P->near_only && P->sweep) throw Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"};
     if (pr.dim < 1 || pr.dim > 3) throw Fail{FFTPIM_VALUE, "dim must be 1, 2 or 3"};
     if (pr.near_order < 1 || pr.near_order > FFTPIM_MAX_ORDER || pr.far_order < 1 ||
         pr.far_order > FFTPIM_MAX_ORDER)
@@ -699,7 +703,7 @@ void build(FftpimPlan* P) {
             jr[a] = 0;
         } else {
             int r = jr_full;
-            if (a < pr.dim) {
+            if (a < pr.dim && pr.i_d >= 1) {
                 int per = (int)std::floor(pr.L[a] / h[a] + 1e-9);
                 int half = (per - 1 >= 0) ? (per - 1) / 2 : -((2 - per) / 2);   // Python floor division
                 r = std::min(r, std::max(half, 1));
@@ -736,7 +740,7 @@ void build(FftpimPlan* P) {
         set_code(0, 0, 0);
         int rng[3][2];
         for (int a = 0; a < 3; ++a) {
-            bool wrap = a < pr.dim && dims[a] > 1;
+            bool wrap = pr.i_d >= 1 && a < pr.dim && dims[a] > 1;
             rng[a][0] = wrap ? -1 : 0;
             rng[a][1] = wrap ? 1 : 0;
         }
@@ -1031,7 +1035,10 @@ void build(FftpimPlan* P) {
 
     // ---- far kernel (farzone.py:100-121, pgf.py:450-462)
     P->far_kernel = dalloc<cplx>(P, prod3(P->far_kdims));
-    P->info.kernel_terms = tabulate_far(P, pr.kshift, im, P->far_kernel, s);
+    if (P->near_only)
+        CK(cudaMemsetAsync(P->far_kernel, 0, sizeof(cplx) * prod3(P->far_kdims), s));
+    else
+        P->info.kernel_terms = tabulate_far(P, pr.kshift, im, P->far_kernel, s);
     // ---- sweep: kernel_hat and far kernel per excitation
     if (P->sweep) {
         const int64_t nk = prod3(P->far_kdims);
@@ -1969,6 +1976,7 @@ int fftpim_nccl_unique_id(void* out, int64_t bytes) {
 int fftpim_group_create(const FftpimProblem* p, int32_t world, int32_t rank, const void* nccl_id,
                         FftpimGroup** out) {
     if (!p || !out || world < 1 || rank < 0 || rank >= world) return fail(Fail{FFTPIM_VALUE, "bad group arguments"});
+    if (p->i_d < 1) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
     *out = nullptr;
     GroupImpl* G = new GroupImpl();
     G->world = world;
@@ -2030,6 +2038,7 @@ void fftpim_group_destroy(FftpimGroup* g) {
 
 int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts, void* stream) {
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (plan->near_only && (parts & FFTPIM_FAR)) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
     if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});
     if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
@@ -2042,6 +2051,7 @@ int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t b
 
 int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts) {
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
+    if (plan->near_only && (parts & FFTPIM_FAR)) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
     if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});
     try {
         CK(cudaSetDevice(plan->device));
@@ -2114,6 +2124,7 @@ int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t pa
                         double* stage_ms) {
     if (!plan || !q || !u || !stage_ms) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "stage profiles are for single-excitation plans"});
+    if (plan->near_only && (parts & FFTPIM_FAR)) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
     cudaEvent_t ev[FFTPIM_N_STAGES + 1] = {};
     try {
         CK(cudaSetDevice(plan->device));

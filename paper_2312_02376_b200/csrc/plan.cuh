@@ -217,6 +217,7 @@ struct FftpimPlan {
     // batched excitation sweep: E phase shifts differing only
     // along periodic axis sw_axis; one pair list with 2 i_d + 1 phase components
     bool sweep = false;
+    bool near_only = false;            // i_d = 0: eval_near only (no far kernel)
     int sw_axis = 0, sw_E = 0, sw_ncomp = 0;
     std::vector<double> sw_k;          // (E, 2) kshift component along sw_axis
     cplx* sw_comp = nullptr;           // (ncomp, P) coefficient components

@@ -5,6 +5,10 @@ by running the REFERENCE's eval_direct / eval_direct_farzone / eval_free_space
 Run in the build container (where /root/reference exists):
     python tests/golden/make_direct_golden.py
 
+Also writes tests/golden/near_id0.npz: build_near_plan with i_d = 0 (the
+near-zone-only plan the reference's bench uses as its free-space baseline,
+cli.py:343-347) and eval_near on small seeded 1D/2D/3D problems.
+
 Writes tests/golden/direct_cases.npz: per case the inputs (positions, charges,
 configuration, policy) and the reference's values, worst_terms and failure
 records (observer, source, 1 = separation | 2 = not converged).  Nothing at run
@@ -89,5 +93,32 @@ def main():
     np.savez_compressed(os.path.join(HERE, "direct_cases.npz"), names=np.array(list(CASES)), **out)
 
 
+def near_id0():
+    from perisum.nearzone import build_near_plan, eval_near
+    out = {}
+    for c, (dim, regime, k0, ks) in enumerate([(1, "npsp", 0.0, (0, 0, 0)), (2, "dynamic", np.pi, (0.3 * np.pi, 0, 0)),
+                                               (3, "dynamic", 2.0, (0.1, 0.2, 0.0))]):
+        rng = np.random.default_rng(300 + c)
+        n = 300
+        pos = rng.uniform(0.0, 1.0, (n, 3))
+        q = rng.standard_normal(n) + (0j if regime == "npsp" else 1j * rng.standard_normal(n))
+        if regime == "npsp":
+            q = q - q.mean()
+        cfg = P.PeriodicityConfig(dim=P.Periodicity(dim), L=(1.0, 1.0, 1.0), k0=complex(k0),
+                                  kshift=tuple(complex(k) for k in ks), regime=P.Regime(regime))
+        params = P.SolverParams(i_d=0, near_grid=(10, 10, 10), near_order=3)
+        plan = build_near_plan(cfg, P.TargetBox((1.0, 1.0, 1.0)), P.SourcePointSet(pos, q), P.ObserverPointSet(pos),
+                               params)
+        u = eval_near(plan, q)
+        key = f"c{c}"
+        out.update({f"{key}__pos": pos, f"{key}__q": q, f"{key}__u": u, f"{key}__dim": dim, f"{key}__regime": regime,
+                    f"{key}__k0": complex(k0), f"{key}__kshift": np.array(ks, dtype=complex),
+                    f"{key}__n_pairs": int(plan.pair_obs.size), f"{key}__n_wrapped": int(plan.n_wrapped_pairs),
+                    f"{key}__join_radius": np.array(plan.join_radius)})
+        print(f"near i_d=0 {key}: pairs={plan.pair_obs.size} wrapped={plan.n_wrapped_pairs} jr={plan.join_radius}")
+    np.savez_compressed(os.path.join(HERE, "near_id0.npz"), **out)
+
+
 if __name__ == "__main__":
     main()
+    near_id0()

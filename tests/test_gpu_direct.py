@@ -127,3 +127,26 @@ def test_fftpim_accuracy_against_direct(fp):
         u = plan.evaluate(q)
         errs.append(float(np.max(np.abs(u - ref.values)) / np.max(np.abs(ref.values))))
     assert errs[1] < errs[0] and errs[1] < 1e-3, errs
+
+
+@pytest.mark.parametrize("key", ["c0", "c1", "c2"])
+def test_near_only_id0_plan_matches_reference(fp, key):
+    """build_near_plan(i_d = 0) + eval_near on the device against the reference
+    (the free-space baseline of the reference's bench, cli.py:343-347); the far
+    engine refuses such a plan like the reference (farzone.py:84-85)."""
+    g = golden("near_id0.npz")
+    c = {k.split("__", 1)[1]: g[k] for k in g.files if k.startswith(key + "__")}
+    regime = {"dynamic": fp.Regime.DYNAMIC, "npsp": fp.Regime.NPSP}[str(c["regime"])]
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(int(c["dim"])), L=(1, 1, 1), k0=complex(c["k0"]),
+                               kshift=tuple(complex(k) for k in c["kshift"]), regime=regime)
+    prm = fp.SolverParams(i_d=0, near_grid=(10, 10, 10), near_order=3)
+    src, obs = fp.SourcePointSet(c["pos"], c["q"]), fp.ObserverPointSet(c["pos"])
+    near = fp.build_near_plan(cfg, fp.TargetBox((1, 1, 1)), src, obs, prm)
+    assert near.native.info.n_pairs == int(c["n_pairs"])
+    assert near.n_wrapped_pairs == 0
+    assert tuple(near.join_radius) == tuple(int(v) for v in c["join_radius"])
+    assert rel_l2(fp.eval_near(near, c["q"]), c["u"]) <= 1e-10
+    with pytest.raises(ValueError):
+        near.native.evaluate(c["q"], fp._native.ALL)
+    with pytest.raises(fp.ValidationError):
+        fp.build_plan(cfg, fp.TargetBox((1, 1, 1)), src, obs, prm)

@@ -42,3 +42,17 @@ def test_free_space_coincident_raises():
     p = np.random.default_rng(0).uniform(size=(5, 3))
     with pytest.raises(ZeroDivisionError):
         free_space(1.0, p, np.ones(5), p)
+
+
+@pytest.mark.parametrize("key", ["c0", "c1", "c2"])
+def test_oracle_near_only_id0_matches_reference(key):
+    """build_near_plan with i_d = 0 (cli.py:343-347 free-space baseline): no
+    wrapped copies, unclipped join radius, free-space near kernel."""
+    from oracle.near_engine import build_near, eval_near
+    g = golden("near_id0.npz")
+    c = {k.split("__", 1)[1]: g[k] for k in g.files if k.startswith(key + "__")}
+    pb = make_problem(int(c["dim"]), k0=complex(c["k0"]), kshift=tuple(c["kshift"]), regime=str(c["regime"]),
+                      i_d=0, near_grid=(10, 10, 10), near_order=3)
+    plan = build_near(pb, c["pos"], c["pos"])
+    assert plan.pair_obs.size == int(c["n_pairs"])
+    assert rel_l2(eval_near(plan, c["q"]), c["u"]) <= 1e-12
