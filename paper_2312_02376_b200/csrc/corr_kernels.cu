@@ -88,35 +88,64 @@ void build_corr_metadata(const int64_t* ptr, int64_t M, int64_t P, int64_t T, un
 #define CORR_WARPS 8
 #endif
 #ifndef CORR_MINB
-#define CORR_MINB 3
+#define CORR_MINB 2
+#endif
+// one tile's streamed data: indices, coefficients, row-start word, segment base
+struct CorrTile {
+    int src[8];
+    double cr[8], ci[8];
+    unsigned word;
+    int64_t sbase;
+};
+
+template <bool REAL>
+__device__ __forceinline__ void corr_load(const EvalArgs& a, int64_t t, int lane, CorrTile& d) {
+    const int64_t T0 = t * CORR_TILE;
+    const int valid = (int)min((int64_t)CORR_TILE, a.n_pairs - T0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int e = 32 * k + lane;
+        const bool ok = e < valid;
+        d.src[k] = ok ? __ldcs(a.pair_src + T0 + e) : 0;
+        if (REAL) {
+            d.cr[k] = ok ? __ldcs(a.coef_r + T0 + e) : 0.0;
+            d.ci[k] = 0.0;
+        } else {
+            const double2 c = ok ? __ldcs(reinterpret_cast<const double2*>(a.coef) + T0 + e) : make_double2(0.0, 0.0);
+            d.cr[k] = c.x;
+            d.ci[k] = c.y;
+        }
+    }
+    // row-start words of the 8 groups: lane k < 8 loads word k, then broadcast per group
+    d.word = lane < 8 ? a.head_bits[(T0 >> 5) + lane] : 0u;
+    d.sbase = a.seg_base[t];
+}
+
+// CORR_PF: the next tile's stream loads are issued before this tile's gathers,
+// so every warp keeps two tiles of pair data in flight
+#ifndef CORR_PF
+#define CORR_PF 1
 #endif
 template <bool REAL>
 __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
-    for (int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp; t < T; t += (int64_t)gridDim.x * CORR_WARPS) {
-        const int64_t T0 = t * CORR_TILE;
-        const int valid = (int)min((int64_t)CORR_TILE, a.n_pairs - T0);
-        // 1. independent loads: indices, coefficients, row-start words, segment base
-        int src[8];
-        double cr[8], ci[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int e = 32 * k + lane;
-            const bool ok = e < valid;
-            src[k] = ok ? __ldcs(a.pair_src + T0 + e) : 0;
-            if (REAL) {
-                cr[k] = ok ? __ldcs(a.coef_r + T0 + e) : 0.0;
-                ci[k] = 0.0;
-            } else {
-                const double2 c = ok ? __ldcs(reinterpret_cast<const double2*>(a.coef) + T0 + e) : make_double2(0.0, 0.0);
-                cr[k] = c.x;
-                ci[k] = c.y;
-            }
+    const int64_t stride = (int64_t)gridDim.x * CORR_WARPS;
+    int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp;
+    CorrTile cur;
+    if (CORR_PF && t < T) corr_load<REAL>(a, t, lane, cur);
+    for (; t < T; t += stride) {
+        CorrTile nxt;
+        if (CORR_PF) {
+            if (t + stride < T) corr_load<REAL>(a, t + stride, lane, nxt);
+        } else {
+            corr_load<REAL>(a, t, lane, cur);
         }
-        // row-start words of the 8 groups: lane k < 8 loads word k, then broadcast per group
-        const unsigned myword = lane < 8 ? a.head_bits[(T0 >> 5) + lane] : 0u;
-        const int64_t sbase = a.seg_base[t];
+        const int* src = cur.src;
+        const double* cr = cur.cr;
+        const double* ci = cur.ci;
+        const unsigned myword = cur.word;
+        const int64_t sbase = cur.sbase;
         // 2. gathers (all 8 in flight)
         double qr[8], qi[8];
 #pragma unroll
@@ -168,6 +197,7 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
         }
         const cplx v = wsum(cplx{accr, acci});
         if (lane == 0) a.seg_val[sbase + seg] = v;
+        if (CORR_PF) cur = nxt;
     }
 }
 
