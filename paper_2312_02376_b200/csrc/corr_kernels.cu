@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
     const int64_t stride = (int64_t)gridDim.x * CORR_WARPS;
     int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp;
+    const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
     CorrTile cur;
     if (CORR_PF && t < T) corr_load<REAL>(a, t, lane, cur);
     for (; t < T; t += stride) {
@@ -153,7 +154,13 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
 #ifdef CORR_NOGATHER   // diagnostic variant: stream-only cost of K4
             const cplx qv = a.q_sorted[(src[k] & 31) + lane];
 #else
-            const cplx qv = a.q_sorted[src[k]];
+            cplx qv;
+            if (realq) {
+                qv.re = a.q_re[src[k]];
+                qv.im = 0.0;
+            } else {
+                qv = a.q_sorted[src[k]];
+            }
 #endif
             qr[k] = qv.re;
             qi[k] = qv.im;

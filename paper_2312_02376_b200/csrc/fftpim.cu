@@ -931,9 +931,13 @@ void build(FftpimPlan* P) {
         P->info.real_coefficients = 0;
     } else {
         launch_code_tables(tb, pg.ncodes, pg, im, tables, tab_total, s);
-        if (P->npsp)
+        if (P->npsp) {
             P->pair_coef_r = dalloc<double>(P, npairs);
-        else
+            if (!P->sharded) {   // real-charge fast path of K4 (eval_kernels.cu k_permute_q)
+                P->q_re = dalloc<double>(P, N);
+                P->q_flag = dalloc<int>(P, 1);
+            }
+        } else
             P->pair_coef = dalloc<cplx>(P, npairs);
         P->info.real_coefficients = P->npsp ? 1 : 0;
         pa.coef = P->pair_coef;
@@ -1141,6 +1145,8 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.pair_src = P->pair_src;
     a.coef = P->pair_coef;
     a.coef_r = P->pair_coef_r;
+    a.q_re = P->q_re;
+    a.q_flag = P->q_flag;
     a.n_pairs = P->info.n_pairs;
     a.head_bits = P->head_bits;
     a.seg_base = P->seg_base;

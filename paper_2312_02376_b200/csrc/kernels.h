@@ -102,6 +102,8 @@ struct EvalArgs {
     const int* src_perm;
     const int* obs_perm;
     cplx* q_sorted;
+    double* q_re;               // NPSP: real parts of q_sorted (null: no real-charge path)
+    int* q_flag;                // nonzero when this evaluation's charges are not all real
     // near
     StencilGeom g;
     int cdims[3];

@@ -130,6 +130,8 @@ struct FftpimPlan {
     cplx* pad_in = nullptr;       // zero-padded projection (corner written each eval)
     cufftHandle fft_plan = 0;
     cplx* q_sorted = nullptr;     // (N) charges permuted to sorted order
+    double* q_re = nullptr;       // (N) their real parts (NPSP plans: K4 gathers 8 B when q is real)
+    int* q_flag = nullptr;        // set by the permutation when some charge has a nonzero imaginary part
     cplx* k1_scratch = nullptr;   // tap-major K1 extended block tiles
     int* k1_cnt = nullptr;        // sliced-ELL K1 (eval_kernels.cu): entries per slot
     int* k1_row = nullptr;        // node of each slot

@@ -114,6 +114,26 @@ def test_batch_and_linearity(fp):
     assert np.array_equal(ub[0], plan.evaluate(q))
 
 
+def test_npsp_real_and_complex_charges(fp):
+    """NPSP plans gather real charges as 8-byte values in K4 when every
+    imaginary part is zero (a per-evaluation device flag); complex charges take
+    the full path.  Both agree with linearity, batches mix the two, and the
+    complex path of a real q (imag = tiny) stays within rounding of it."""
+    plan, q = _full(fp, 1)
+    q = np.ascontiguousarray(q.real + 0j)
+    rng = np.random.default_rng(8)
+    qi = rng.standard_normal(q.size)
+    qi -= qi.mean()
+    u_re, u_im = plan.evaluate(q), plan.evaluate(qi + 0j)
+    u_c = plan.evaluate(q + 1j * qi)
+    assert rel_l2(u_c, u_re + 1j * u_im) <= 1e-13
+    ub = plan.evaluate(np.stack([q, q + 1j * qi, q]))
+    assert np.array_equal(ub[0], u_re) and np.array_equal(ub[2], u_re)
+    assert rel_l2(ub[1], u_c) <= 1e-15
+    g = golden("c1_full.npz")
+    assert rel_l2(u_re, g["u"]) <= 1e-10
+
+
 def test_oracle_parity_random_cases(fp):
     """Fresh seeded instances (not in the golden set) against the CPU oracle."""
     from oracle.pipeline import build_plan as oracle_build
