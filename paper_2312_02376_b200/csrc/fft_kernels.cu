@@ -320,7 +320,7 @@ static bool launch_fft_stage_p2(const FftStage& st, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------
 // Register-resident column FFTs, L = E * T with E = 16 values per thread and
-// T = L / 16 threads per column (L = 64, 128, 256).  Thread t of a column holds
+// T = L / 16 threads per column (L = 64, 128, 256), E = 32 and T = 16 for L = 512.  Thread t of a column holds
 // x[t + T j] (j < E); the transform is the two-level split
 //   X[k1 + E k2] = sum_t w_T^{t k2} w_L^{t k1} sum_j x[t + T j] w_E^{j k1}
 // -- an E-point DFT in registers, the twiddle, one shared-memory exchange and
@@ -401,9 +401,16 @@ __device__ __forceinline__ cplx twl(const cplx* __restrict__ tw, int m) {
     return SIGN < 0 ? cplx{w.x, w.y} : cplx{w.x, -w.y};
 }
 
+// values per thread: 16 for L <= 256, 32 for L = 512 (T = L / E threads per
+// column; the second level needs T | E)
+template <int L>
+struct RegE {
+    static constexpr int E = L <= 256 ? 16 : 32;
+};
+
 template <int L, int SIGN>
-__device__ __forceinline__ void reg_fwd(cplx (&a)[16], cplx* buf, int t, const cplx* tw) {
-    constexpr int E = 16, T = L / E;
+__device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
+    constexpr int E = RegE<L>::E, T = L / E;
     dft_reg<E, SIGN>(a);
 #pragma unroll
     for (int k1 = 1; k1 < E; ++k1) a[k1] = a[k1] * twl<SIGN>(tw, (t * k1) & (L - 1));
@@ -424,8 +431,8 @@ __device__ __forceinline__ void reg_fwd(cplx (&a)[16], cplx* buf, int t, const c
 
 // inverse of the layout reg_fwd leaves (unnormalised, sign +1)
 template <int L>
-__device__ __forceinline__ void reg_inv(cplx (&a)[16], cplx* buf, int t, const cplx* tw) {
-    constexpr int E = 16, T = L / E;
+__device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
+    constexpr int E = RegE<L>::E, T = L / E;
     __syncthreads();   // buf reuse
 #pragma unroll
     for (int s = 0; s < E / T; ++s) {
@@ -447,7 +454,7 @@ __device__ __forceinline__ void reg_inv(cplx (&a)[16], cplx* buf, int t, const c
 #define RF_THREADS 128
 template <int L, bool ZC>
 __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
-    constexpr int E = 16, T = L / E, CPB = RF_THREADS / T, CS = E * (T + 1) + 1;
+    constexpr int E = RegE<L>::E, T = L / E, CPB = RF_THREADS / T, CS = E * (T + 1) + 1;
     extern __shared__ cplx xs[];
     const int c = ZC ? threadIdx.x / T : threadIdx.x % CPB;
     const int t = ZC ? threadIdx.x % T : threadIdx.x / CPB;
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
 template <int L>
 static bool reg_launch(const FftStage& st, cudaStream_t s) {
     if (st.L != L) return false;
-    constexpr int T = L / 16, CPB = RF_THREADS / T, CS = 16 * (T + 1) + 1;
+    constexpr int E = RegE<L>::E, T = L / E, CPB = RF_THREADS / T, CS = E * (T + 1) + 1;
     const size_t smem = (size_t)CPB * CS * sizeof(cplx);
     static bool configured = false;
     if (!configured) {
@@ -528,7 +535,12 @@ static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
         return e && e[0] == '0';
     }();
     if (off) return false;
-    return reg_launch<64>(st, s) || reg_launch<128>(st, s) || reg_launch<256>(st, s);
+    static const bool r512 = [] {
+        const char* e = getenv("FFTPIM_FFT_REG512");
+        return !(e && e[0] == '0');
+    }();
+    return reg_launch<64>(st, s) || reg_launch<128>(st, s) || reg_launch<256>(st, s) ||
+           (r512 && reg_launch<512>(st, s));
 }
 
 size_t fft_stage_smem(const FftStage& st) { return (size_t)(2 * st.B * (st.L + 1) + st.L + st.ntwp) * sizeof(cplx); }
