@@ -286,8 +286,9 @@ def run_b200(args):
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes": nbytes[dom], "kernel_ms": prof[dom]},
             "stages_ms": prof,
-            "schedule": "batched precorrection (FP64-bound) on a low-priority stream, per-excitation "
-                        "chains on a high-priority stream, then one K4-sum pass",
+            "schedule": ("one CUDA graph: near chain (high-priority stream) | K4 (low priority, capped grid) | "
+                         "far chain, split observer pass" if int(info.n_pairs) <= 500_000_000 else
+                         "chains in order (K4 uses the whole chip)"),
             "stage_gbs": {k: nbytes[k] / (prof[k] * 1e-3) / 1e9 for k in nbytes if prof.get(k, 0) > 0},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * w.n_points,
                     "d2h_bytes_per_step": 16 * w.n_points},

@@ -232,6 +232,9 @@ __device__ __forceinline__ double2 ld_d2(const cplx* p) {
 #ifndef K1E_THREADS
 #define K1E_THREADS 256
 #endif
+#ifndef K1_PF
+#define K1_PF 1
+#endif
 __global__ void __launch_bounds__(K1E_THREADS, 1) k_k1_spmv(EvalArgs a) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int n1 = a.g.n[1], n2 = a.g.n[2];
@@ -244,6 +247,48 @@ __global__ void __launch_bounds__(K1E_THREADS, 1) k_k1_spmv(EvalArgs a) {
     const cplx* q = a.k1_q;
     double ar = 0.0, ai = 0.0;
     int g = 0;
+#if K1_PF
+    // the next pair of groups' indices and weights are in flight while this
+    // pair's q gathers complete (same entry order: identical sums)
+    int4 i0, i1;
+    double2 w0, w1, w2, w3;
+    if (G >= 2) {
+        i0 = ld_cs_i4(ix);
+        i1 = ld_cs_i4(ix + 128);
+        w0 = ld_cs_d2(wt);
+        w1 = ld_cs_d2(wt + 2);
+        w2 = ld_cs_d2(wt + 128);
+        w3 = ld_cs_d2(wt + 128 + 2);
+    }
+    for (; g + 2 <= G; g += 2) {
+        int4 j0 = i0, j1 = i1;
+        double2 x0 = w0, x1 = w1, x2 = w2, x3 = w3;
+        if (g + 4 <= G) {
+            j0 = ld_cs_i4(ix + 128 * (g + 2));
+            j1 = ld_cs_i4(ix + 128 * (g + 3));
+            x0 = ld_cs_d2(wt + 128 * (g + 2));
+            x1 = ld_cs_d2(wt + 128 * (g + 2) + 2);
+            x2 = ld_cs_d2(wt + 128 * (g + 3));
+            x3 = ld_cs_d2(wt + 128 * (g + 3) + 2);
+        }
+        const double2 v0 = ld_d2(q + i0.x), v1 = ld_d2(q + i0.y), v2 = ld_d2(q + i0.z), v3 = ld_d2(q + i0.w);
+        const double2 v4 = ld_d2(q + i1.x), v5 = ld_d2(q + i1.y), v6 = ld_d2(q + i1.z), v7 = ld_d2(q + i1.w);
+        ar += w0.x * v0.x; ai += w0.x * v0.y;
+        ar += w0.y * v1.x; ai += w0.y * v1.y;
+        ar += w1.x * v2.x; ai += w1.x * v2.y;
+        ar += w1.y * v3.x; ai += w1.y * v3.y;
+        ar += w2.x * v4.x; ai += w2.x * v4.y;
+        ar += w2.y * v5.x; ai += w2.y * v5.y;
+        ar += w3.x * v6.x; ai += w3.x * v6.y;
+        ar += w3.y * v7.x; ai += w3.y * v7.y;
+        i0 = j0;
+        i1 = j1;
+        w0 = x0;
+        w1 = x1;
+        w2 = x2;
+        w3 = x3;
+    }
+#else
     for (; g + 2 <= G; g += 2) {
         const int4 i0 = ld_cs_i4(ix + 128 * g), i1 = ld_cs_i4(ix + 128 * (g + 1));
         const double2 w0 = ld_cs_d2(wt + 128 * g), w1 = ld_cs_d2(wt + 128 * g + 2);
@@ -259,6 +304,7 @@ __global__ void __launch_bounds__(K1E_THREADS, 1) k_k1_spmv(EvalArgs a) {
         ar += w3.x * v6.x; ai += w3.x * v6.y;
         ar += w3.y * v7.x; ai += w3.y * v7.y;
     }
+#endif
     if (g < G) {
         const int4 i0 = ld_cs_i4(ix + 128 * g);
         const double2 w0 = ld_cs_d2(wt + 128 * g), w1 = ld_cs_d2(wt + 128 * g + 2);

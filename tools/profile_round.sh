@@ -1,9 +1,10 @@
 #!/usr/bin/env bash
 # Round-end evidence on one B200 (run through gpurun from the repo root):
-#   bench lines for every config, the reference arm for the default config,
-#   the ncu launch list of the default bench command and one `--set full`
-#   capture of the evaluation kernels.  Each ncu pass runs only after the same
-#   command exited 0 without ncu.  Outputs land in gpurun_out/round/.
+#   bench lines for every config (C5 both as the 64-excitation sweep and per
+#   excitation), the reference arm for the default config, the ncu launch list
+#   of the default bench command and one `--set full` capture of the
+#   evaluation kernels.  Each ncu pass runs only after the same command exited
+#   0 without ncu.  Outputs land in gpurun_out/round/.
 set -u
 OUT=gpurun_out/round
 mkdir -p $OUT
@@ -12,6 +13,7 @@ python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.jsonl 2> 
 for c in 1 3 4 5; do
   python bench.py --config $c --steps 10 --warmup 3 > $OUT/bench_c$c.jsonl 2> $OUT/bench_c$c.err; echo "bench c$c rc=$?"
 done
+python bench.py --config 5 --per-excitation --steps 10 --warmup 3 > $OUT/bench_c5pe.jsonl 2> $OUT/bench_c5pe.err; echo "bench c5pe rc=$?"
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 export FFTPIM_NO_GRAPHS=1
 if timeout 300 $CMD > $OUT/plain.log 2>&1; then
