@@ -1204,7 +1204,93 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
 // plan-owned streams after the q permutation (K4 streams HBM while the FFT
 // stages are latency-bound) and join before the observer pass; for very large
 // pair streams (C3/C4) K4 needs the whole chip and the chains run in order.
+// ---------------------------------------------------------------------------
+// Multi-RHS batches (batch >= FFTPIM_BATCH_MIN charge vectors on one plan): the
+// correction pairs stream ONCE per 64 right-hand sides through the batched
+// row kernel of the sweep (sweep_kernels.cu, one component, unit phases)
+// instead of once per vector; the per-vector chains (far chain, K1, FFT stages,
+// observer pass without the K4 term) follow, then one pass adds the K4 sums.
+static int batch_min() {
+    static const int v = [] {
+        const char* e = getenv("FFTPIM_BATCH_MIN");
+        return e ? atoi(e) : 8;
+    }();
+    return v;
+}
+
+static bool batched_k4(const FftpimPlan* P, int64_t batch, int parts) {
+    return batch >= batch_min() && (parts & FFTPIM_NEAR) && P->pair_coef && !P->sweep && !P->sharded &&
+           P->N < ((int64_t)1 << 30) && P->info.n_pairs > 0;
+}
+
+// device buffers of the batched path, allocated outside any graph capture
+static void ensure_batch_buffers(FftpimPlan* P, int64_t batch, int parts) {
+    if (!batched_k4(P, batch, parts)) return;
+    int E = (int)std::min<int64_t>(64, batch);
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    while (E > 8 && (size_t)(P->N + P->M) * E * sizeof(cplx) > fr / 2) E /= 2;
+    if (P->bt_E >= E) return;
+    dfree(P, P->bt_qt);
+    dfree(P, P->bt_corr);
+    dfree(P, P->bt_omega);
+    P->bt_qt = dalloc<cplx>(P, P->N * E);
+    P->bt_corr = dalloc<cplx>(P, P->M * E);
+    std::vector<cplx> ones((size_t)3 * E, cplx{1.0, 0.0});
+    P->bt_omega = dalloc<cplx>(P, 3 * E);
+    CK(cudaMemcpy(P->bt_omega, ones.data(), sizeof(cplx) * ones.size(), cudaMemcpyHostToDevice));
+    P->bt_E = E;
+    if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);   // captured with the old buffers
+    P->graph_exec = nullptr;
+}
+
+static void evaluate_batched(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s) {
+    cudaStream_t sn = P->aux[0], sc = P->aux[1];
+    if (parts & FFTPIM_NEAR && !P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, sn));
+    for (int64_t b0 = 0; b0 < batch; b0 += P->bt_E) {
+        const int E = (int)std::min<int64_t>(P->bt_E, batch - b0);
+        const double* qb = q + 2 * b0 * P->N;
+        double* ub = u + 2 * b0 * P->M;
+        CK(cudaEventRecord(P->ev_fork, s));
+        CK(cudaStreamWaitEvent(sn, P->ev_fork, 0));
+        CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
+        launch_batch_permute((const cplx*)qb, P->src_perm, P->N, E, P->bt_qt, sc);
+        launch_corr_sweep(P->pair_ptr, P->pair_src, P->pair_coef, 1, P->info.n_pairs, P->bt_qt, P->N, E, P->bt_omega,
+                          P->bt_corr, P->M, sc);
+        for (int e = 0; e < E; ++e) {
+            EvalArgs a = eval_args(P, qb + 2 * (int64_t)e * P->N, ub + 2 * (int64_t)e * P->M, parts);
+            a.sw_e = -1;   // the K4 term is added below
+            launch_permute_q(a, sn);
+            if (parts & FFTPIM_FAR) {
+                launch_far_project(a, sn);
+                launch_far_sum(a, sn);
+            }
+            launch_near_project(a, sn);
+            if (P->custom_fft) {
+                for (int k = 0; k < 5; ++k)
+                    if (P->stage_on[k]) launch_fft_stage(P->stage[k], sn);
+            } else {
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+                launch_spectrum_mul(a, sn);
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+                fftpim_count_launch(2);
+            }
+            launch_observers(a, sn);
+        }
+        CK(cudaEventRecord(P->ev_join[0], sn));
+        CK(cudaEventRecord(P->ev_join[1], sc));
+        CK(cudaStreamWaitEvent(s, P->ev_join[0], 0));
+        CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));
+        launch_sweep_add_corr((cplx*)ub, P->bt_corr, P->obs_perm, P->M, E, s);
+    }
+    CK(cudaGetLastError());
+}
+
 void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s) {
+    if (batched_k4(P, batch, parts) && P->bt_E > 0) {
+        evaluate_batched(P, q, u, batch, parts, s);
+        return;
+    }
     const bool concurrent = P->info.n_pairs <= 500000000LL;
     if (!concurrent) {
         if (parts & FFTPIM_NEAR && !P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
@@ -1309,6 +1395,7 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
               cudaEvent_t* ev = nullptr) {
     if (parts & ~FFTPIM_ALL || parts == 0) throw Fail{FFTPIM_VALUE, "parts must be a non-empty subset of NEAR|FAR"};
     CK(cudaSetDevice(P->device));
+    if (!ev) ensure_batch_buffers(P, batch, parts);
     if (!ev && P->use_graphs) {
         // replay a captured CUDA graph of the whole evaluation (launch-bound at small N);
         // re-captured whenever the caller's buffers or the batch change.  The

@@ -227,6 +227,10 @@ struct FftpimPlan {
     bool serial_sweep_required = getenv("FFTPIM_SWEEP_SERIAL") != nullptr;   // diagnostics: one stream
     cplx* sw_khat = nullptr;           // (E, n_fft) kernel_hat per excitation
     cplx* sw_far = nullptr;            // (E, nk) far kernel per excitation
+    int bt_E = 0;                      // multi-RHS batches: right-hand sides per batched K4 pass
+    cplx* bt_qt = nullptr;             // (N, bt_E) sorted charges, right-hand side fastest
+    cplx* bt_corr = nullptr;           // (M, bt_E) batched K4 sums
+    cplx* bt_omega = nullptr;          // (bt_E, 3) ones: unit phases for the one-component sweep kernel
     cplx* sw_omega = nullptr;          // (E, ncomp + 2) exp(-j m k_e L), m = -(i_d+1) .. i_d+1
     cplx* sw_qt = nullptr;             // (N, E) sorted charges, excitation fastest
     cplx* sw_corr = nullptr;           // (M, E) batched K4 sums, excitation fastest

@@ -178,12 +178,30 @@ void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp
         k_corr_sweep<NC, false, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M); \
     else                                                                                                         \
         k_corr_sweep<NC, false, false><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M);
-    if (ncomp == 3) {
+    if (ncomp == 1) {
+        KS(1)
+    } else if (ncomp == 3) {
         KS(3)
     } else {
         KS(5)
     }
 #undef KS
+    fftpim_count_launch();
+}
+
+// multi-RHS batches on one plan: qt[i][e] = q[e][perm[i]] (no phases)
+__global__ void k_batch_permute(const cplx* __restrict__ q, const int* __restrict__ perm, int64_t N, int E,
+                                cplx* __restrict__ qt) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N * E) return;
+    const int64_t i = t / E;
+    const int e = (int)(t - i * E);
+    qt[t] = q[(int64_t)e * N + perm[i]];
+}
+
+void launch_batch_permute(const cplx* q, const int* perm, int64_t N, int E, cplx* qt, cudaStream_t s) {
+    if (N == 0) return;
+    k_batch_permute<<<nblk(N * E, 256), 256, 0, s>>>(q, perm, N, E, qt);
     fftpim_count_launch();
 }
 

@@ -114,6 +114,26 @@ def test_batch_and_linearity(fp):
     assert np.array_equal(ub[0], plan.evaluate(q))
 
 
+@pytest.mark.parametrize("B", [12, 70])
+def test_multi_rhs_batch_matches_single_evaluations(fp, B):
+    """Batches of >= 8 charge vectors stream the correction pairs once per 64
+    right-hand sides (batched K4 + per-vector chains); every row equals the
+    single-vector evaluation to rounding, both through the host and device entry."""
+    import torch
+    plan, q = _full(fp, 2)
+    rng = np.random.default_rng(B)
+    Q = rng.standard_normal((B, q.size)) + 1j * rng.standard_normal((B, q.size))
+    U = plan.evaluate(Q)
+    for b in (0, 5, B - 1):
+        assert rel_l2(U[b], plan.evaluate(Q[b])) <= 1e-13, b
+    Ud = plan.evaluate(torch.from_numpy(Q).cuda()).cpu().numpy()
+    assert np.array_equal(U, Ud)
+    assert np.array_equal(U, plan.evaluate(Q))          # bitwise reproducible
+    g = golden("c2_full.npz")
+    Q[3] = q
+    assert rel_l2(plan.evaluate(Q)[3], g["u"]) <= 1e-10
+
+
 def test_npsp_real_and_complex_charges(fp):
     """NPSP plans gather real charges as 8-byte values in K4 when every
     imaginary part is zero (a per-evaluation device flag); complex charges take
