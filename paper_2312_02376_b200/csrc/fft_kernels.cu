@@ -408,12 +408,14 @@ struct RegE {
     static constexpr int E = L <= 256 ? 16 : 32;
 };
 
-template <int L, int SIGN>
+// TS: stride into the twiddle table (1: tw has L entries; 3: tw is the table
+// of a length-3L transform, w_L^m = tw[3 m])
+template <int L, int SIGN, int TS = 1>
 __device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
     constexpr int E = RegE<L>::E, T = L / E;
     dft_reg<E, SIGN>(a);
 #pragma unroll
-    for (int k1 = 1; k1 < E; ++k1) a[k1] = a[k1] * twl<SIGN>(tw, (t * k1) & (L - 1));
+    for (int k1 = 1; k1 < E; ++k1) a[k1] = a[k1] * twl<SIGN>(tw, ((t * k1) & (L - 1)) * TS);
 #pragma unroll
     for (int k1 = 0; k1 < E; ++k1) buf[k1 * (T + 1) + t] = a[k1];
     __syncthreads();
@@ -430,7 +432,7 @@ __device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t,
 }
 
 // inverse of the layout reg_fwd leaves (unnormalised, sign +1)
-template <int L>
+template <int L, int TS = 1>
 __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
     constexpr int E = RegE<L>::E, T = L / E;
     __syncthreads();   // buf reuse
@@ -443,7 +445,7 @@ __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t,
         dft_reg<T, +1>(b);
         cplx* row = buf + k1 * (T + 1);
 #pragma unroll
-        for (int n2 = 0; n2 < T; ++n2) row[n2] = n2 ? b[n2] * twl<+1>(tw, (k1 * n2) & (L - 1)) : b[n2];
+        for (int n2 = 0; n2 < T; ++n2) row[n2] = n2 ? b[n2] * twl<+1>(tw, ((k1 * n2) & (L - 1)) * TS) : b[n2];
     }
     __syncthreads();
 #pragma unroll
@@ -529,6 +531,121 @@ static bool reg_launch(const FftStage& st, cudaStream_t s) {
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// L = 3 M (M = 32 .. 256: L = 96, 192, 384, 768) register-resident column FFTs
+// by one radix-3 split in frequency:
+//   X[3k + r] = FFT_M(y_r)[k],   y_r[n] = w_L^(s n r) sum_m x[n + m M] w_3^(s m r)
+// A column has 3 T threads (T = M / 16): thread (r, t) builds y_r[t + T j]
+// (j < 16) from its three input rows and runs group r's M-point register FFT
+// (reg_fwd with the L table at stride 3).  The inverse of the fused x stage
+// runs the group FFTs backwards (reg_inv) and recombines the groups through
+// shared memory:  x[n + m M] = sum_r w_3^(m r) w_L^(n r) z_r[n].
+#define RF3_THREADS 192
+template <int SIGN>
+__device__ __forceinline__ cplx w3pow(int e) {   // exp(SIGN 2 pi i e / 3)
+    const double h = 0.86602540378443864676;
+    switch (e % 3) {
+        case 0: return cplx{1.0, 0.0};
+        case 1: return cplx{-0.5, SIGN < 0 ? -h : h};
+        default: return cplx{-0.5, SIGN < 0 ? h : -h};
+    }
+}
+
+template <int M, int SIGN>
+__device__ __forceinline__ void reg3_split(cplx (&a)[16], const cplx* __restrict__ in, int64_t stride, int lin,
+                                           bool okc, int r, int t, const cplx* tw) {
+    constexpr int L = 3 * M, T = M / 16;
+    const cplx w1 = w3pow<SIGN>(r), w2 = w3pow<SIGN>(2 * r);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int n = t + T * j;
+        const cplx v0 = (okc && n < lin) ? in[(int64_t)n * stride] : mk(0.0);
+        const cplx v1 = (okc && n + M < lin) ? in[(int64_t)(n + M) * stride] : mk(0.0);
+        const cplx v2 = (okc && n + 2 * M < lin) ? in[(int64_t)(n + 2 * M) * stride] : mk(0.0);
+        const cplx y = v0 + w1 * v1 + w2 * v2;
+        a[j] = r ? y * twl<SIGN>(tw, (n * r) % L) : y;
+    }
+}
+
+template <int M, bool ZC>
+__global__ void __launch_bounds__(RF3_THREADS) k_fft_reg3(FftStage st) {
+    constexpr int L = 3 * M, E = 16, T = M / E, TPC = 3 * T, CPB = RF3_THREADS / TPC, CS = E * (T + 1) + 1;
+    constexpr int COLS = 3 * CS > L ? 3 * CS : L;   // shared words per column
+    extern __shared__ cplx xs[];
+    const int c = ZC ? threadIdx.x / TPC : threadIdx.x % CPB;
+    const int u = ZC ? threadIdx.x % TPC : threadIdx.x / CPB;
+    const int r = u / T, t = u % T;
+    const int col = blockIdx.x * CPB + c;
+    const bool okc = col < st.nb0;
+    const cplx* __restrict__ in = st.in + (int64_t)blockIdx.y * st.in_s1 + (int64_t)col * st.in_s0;
+    cplx* out = st.out + (int64_t)blockIdx.y * st.out_s1 + (int64_t)col * st.out_s0;
+    cplx* cbuf = xs + c * COLS;
+    cplx* buf = cbuf + r * CS;
+    cplx a[E];
+    if (st.spec) {
+        reg3_split<M, -1>(a, in, st.in_stride, st.lin, okc, r, t, st.tw);
+        reg_fwd<M, -1, 3>(a, buf, t, st.tw);
+        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + (int64_t)col * st.spec_s0;
+        if (okc) {
+#pragma unroll
+            for (int s2 = 0; s2 < E / T; ++s2)
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2)
+                    a[s2 * T + k2] = a[s2 * T + k2] * sp[(int64_t)(3 * (t + T * s2 + E * k2) + r) * st.spec_stride];
+        }
+        reg_inv<M, 3>(a, buf, t, st.tw);
+        // recombine: thread (m, t) produces x[n + m M] from the three groups' z_r[n]
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const int n = t + T * j;
+            cbuf[r * M + n] = r ? a[j] * twl<+1>(st.tw, (n * r) % L) : a[j];
+        }
+        __syncthreads();
+        const cplx w1 = w3pow<+1>(r), w2 = w3pow<+1>(2 * r);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const int n = t + T * j, i = n + r * M;
+            if (okc && i < st.lout) out[(int64_t)i * st.out_stride] = cbuf[n] + w1 * cbuf[M + n] + w2 * cbuf[2 * M + n];
+        }
+        return;
+    }
+    if (st.sign < 0) {
+        reg3_split<M, -1>(a, in, st.in_stride, st.lin, okc, r, t, st.tw);
+        reg_fwd<M, -1, 3>(a, buf, t, st.tw);
+    } else {
+        reg3_split<M, +1>(a, in, st.in_stride, st.lin, okc, r, t, st.tw);
+        reg_fwd<M, +1, 3>(a, buf, t, st.tw);
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < E / T; ++s2)
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) {
+            const int k = 3 * (t + T * s2 + E * k2) + r;
+            if (okc && k < st.lout) out[(int64_t)k * st.out_stride] = a[s2 * T + k2];
+        }
+}
+
+template <int M>
+static bool reg3_launch(const FftStage& st, cudaStream_t s) {
+    if (st.L != 3 * M) return false;
+    constexpr int L = 3 * M, T = M / 16, TPC = 3 * T, CPB = RF3_THREADS / TPC, CS = 16 * (T + 1) + 1;
+    constexpr int COLS = 3 * CS > L ? 3 * CS : L;
+    const size_t smem = (size_t)CPB * COLS * sizeof(cplx);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_fft_reg3<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_reg3<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid((st.nb0 + CPB - 1) / CPB, st.nb1);
+    if (st.in_stride == 1)
+        k_fft_reg3<M, true><<<grid, RF3_THREADS, smem, s>>>(st);
+    else
+        k_fft_reg3<M, false><<<grid, RF3_THREADS, smem, s>>>(st);
+    return true;
+}
+
 static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
     static const bool off = [] {
         const char* e = getenv("FFTPIM_FFT_REG");
@@ -539,8 +656,14 @@ static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
         const char* e = getenv("FFTPIM_FFT_REG512");
         return !(e && e[0] == '0');
     }();
+    static const bool r3 = [] {
+        const char* e = getenv("FFTPIM_FFT_REG3");
+        return !(e && e[0] == '0');
+    }();
     return reg_launch<64>(st, s) || reg_launch<128>(st, s) || reg_launch<256>(st, s) ||
-           (r512 && reg_launch<512>(st, s));
+           (r512 && reg_launch<512>(st, s)) ||
+           (r3 && (reg3_launch<32>(st, s) || reg3_launch<64>(st, s) || reg3_launch<128>(st, s) ||
+                   reg3_launch<256>(st, s)));
 }
 
 size_t fft_stage_smem(const FftStage& st) { return (size_t)(2 * st.B * (st.L + 1) + st.L + st.ntwp) * sizeof(cplx); }

@@ -44,6 +44,15 @@ def main():
                                    regime=fp.Regime("npsp"))
         box, obs = fp.TargetBox((1, 1, 1)), pos
         prm = fp.SolverParams(near_grid=(20, 20, 20), near_order=3, far_grid=(6, 6, 6))
+    elif case == "tri":
+        # doubled dims 96, 384, 24: the L = 3 * 2^k register FFTs (96, 384) and a Stockham axis
+        rng = np.random.default_rng(31)
+        pos = rng.uniform(0.0, 1.0, (3000, 3)) * np.array([1.0, 1.0, 0.25])
+        q = rng.standard_normal(3000) + 1j * rng.standard_normal(3000)
+        cfg = fp.PeriodicityConfig(dim=fp.Periodicity(2), L=(1, 1, 1), k0=1.5 * np.pi - 0.2j,
+                                   kshift=(0.3, 0.1, 0), regime=fp.Regime("dynamic"))
+        box, obs = fp.TargetBox((1, 1, 0.25)), pos
+        prm = fp.SolverParams(near_grid=(48, 192, 12), near_order=3, far_grid=(6, 6, 4))
     else:
         from cases import SMALL_CASES, case_inputs, regime_of
         d = SMALL_CASES[case]

@@ -49,10 +49,13 @@ def test_k1_ell_matches_computed_projection(case, tmp_path):
         assert rel_l2(u_ell, u_tap) <= 1e-13
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d"])
+@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d", "tri"])
 def test_register_fft_matches_stockham_and_cufft(case, tmp_path):
     u_reg, _ = run_variant(case, {}, tmp_path, "reg")
     u_smem, _ = run_variant(case, {"FFTPIM_FFT_REG": "0"}, tmp_path, "smem")
+    if case == "tri":   # the radix-3 register kernels alone switched off
+        u_r3, _ = run_variant(case, {"FFTPIM_FFT_REG3": "0"}, tmp_path, "noreg3")
+        assert rel_l2(u_reg, u_r3) <= 1e-13
     u_cufft, i_cufft = run_variant(case, {"FFTPIM_FFT": "cufft"}, tmp_path, "cufft")
     assert not i_cufft["custom_fft"]
     assert rel_l2(u_reg, u_smem) <= 1e-13
