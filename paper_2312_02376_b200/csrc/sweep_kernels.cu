@@ -169,23 +169,6 @@ void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp
                        const cplx* qt3, int64_t N, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s) {
     if (M == 0) return;
     const int blocks = nblk(M * 32, 256);
-    // shared-memory carveout of the batched K4 (percent; -1 = driver default).
-    // SMs keep a kernel's carveout while its blocks run, so a large carveout
-    // lets the per-excitation chain kernels (up to ~130 KB of shared memory)
-    // start on SMs as K4 blocks retire.
-    static const int carve = [] {
-        const char* e = getenv("FFTPIM_SWEEP_CARVEOUT");
-        return e ? atoi(e) : -1;
-    }();
-    if (carve >= 0) {
-        static bool set = false;
-        if (!set) {
-            cudaFuncSetAttribute(k_corr_sweep<1, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-            cudaFuncSetAttribute(k_corr_sweep<3, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-            cudaFuncSetAttribute(k_corr_sweep<5, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-            set = true;
-        }
-    }
 #define KS(NC)                                                                                                   \
     if (E == 64)                                                                                                 \
         k_corr_sweep<NC, true, true><<<blocks, 256, 0, s>>>(ptr, pair_src, comp, P, qt3, N, E, omega, corr, M); \

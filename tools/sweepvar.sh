@@ -1,0 +1,9 @@
+mkdir -p gpurun_out/s18
+L=paper_2312_02376_b200/lib
+timeout 600 python -m pytest tests/test_gpu_sweep.py tests/test_gpu_parity.py -k "sweep or multi_rhs" -x -q > gpurun_out/s18/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/s18/pytest.log
+for v in default wpo1 wpo2 wpo8; do
+  if [ $v = default ]; then lib=$L/libfftpim.so; else lib=$L/variants/libfftpim_$v.so; fi
+  FFTPIM_LIB=$lib timeout 600 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/s18/c5_$v.jsonl 2> gpurun_out/s18/c5_$v.err
+  echo "c5 $v rc=$?"
+  FFTPIM_LIB=$lib timeout 600 python tools/batch_bench.py --config 5 --batch 64 --reps 2 > gpurun_out/s18/b5_$v.json 2>&1; tail -1 gpurun_out/s18/b5_$v.json | cut -c1-150
+done
