@@ -500,6 +500,16 @@ static int64_t tabulate_far(FftpimPlan* P, const double ks[3][2], const ImageSet
     return st.kernel_terms;
 }
 
+// plans with at most this many pairs run the concurrent schedule (near chain |
+// K4 | far chain); larger ones run the stages in order (FFTPIM_CONCURRENT_MAX)
+static int64_t concurrent_max_pairs() {
+    static const int64_t v = [] {
+        const char* e = getenv("FFTPIM_CONCURRENT_MAX");
+        return e ? (int64_t)atoll(e) : (int64_t)500000000LL;
+    }();
+    return v;
+}
+
 void build(FftpimPlan* P) {
     const FftpimProblem& pr = P->prob;
     cudaStream_t s = P->build_stream;
@@ -1091,7 +1101,7 @@ void build(FftpimPlan* P) {
         P->far_qg = dalloc<cplx>(P, nf);
         P->far_ug = dalloc<cplx>(P, nf);
     }
-    if (npairs <= 500000000LL && getenv("FFTPIM_OBS_FUSED") == nullptr)
+    if (npairs <= concurrent_max_pairs() && getenv("FFTPIM_OBS_FUSED") == nullptr)
         P->obs_pre = dalloc<cplx>(P, Mown);   // split observer pass (concurrent schedule)
     CK(cudaStreamSynchronize(s));
     dfree(P, d_cnt);
@@ -1291,7 +1301,7 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         evaluate_batched(P, q, u, batch, parts, s);
         return;
     }
-    const bool concurrent = P->info.n_pairs <= 500000000LL;
+    const bool concurrent = P->info.n_pairs <= concurrent_max_pairs();
     if (!concurrent) {
         if (parts & FFTPIM_NEAR && !P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
         for (int64_t b = 0; b < batch; ++b) {
