@@ -1339,12 +1339,16 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         // split observer pass: far interpolation + K4 fix-up run off the near
         // chain; the final pass after the inverse FFT only interpolates the near grid
         const bool split = parts == FFTPIM_ALL && P->obs_pre != nullptr;
-        if (parts & FFTPIM_FAR) {
+        // capture order = the order the graph hands ready kernels to the GPU:
+        // the near chain (critical path) first, then the far chain, then K4
+        auto far_chain = [&]() {
+            if (!(parts & FFTPIM_FAR)) return;
             CK(cudaStreamWaitEvent(sf, P->ev_fork, 0));
             launch_far_project(a, sf);
             launch_far_sum(a, sf);
             CK(cudaEventRecord(P->ev_join[2], sf));
-        }
+        };
+        if (!(parts & FFTPIM_NEAR)) far_chain();
         if (parts & FFTPIM_NEAR) {
             CK(cudaStreamWaitEvent(sn, P->k1_orig ? P->ev_start : P->ev_fork, 0));
             launch_near_project(a, sn);
@@ -1366,14 +1370,16 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
                 fftpim_count_launch(2);
             }
             CK(cudaEventRecord(P->ev_join[0], sn));
+            far_chain();
             CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
             if (k4_gate && P->custom_fft) CK(cudaStreamWaitEvent(sc, P->ev_k1, 0));
             {
                 // K4 streams HBM on part of the chip while the latency-bound
-                // near chain runs on the rest (FFTPIM_CORR_BLOCKS tunes the split)
+                // near chain runs on the rest (FFTPIM_CORR_BLOCKS tunes the split;
+                // its persistent blocks hold the register file, 1.5 per SM measured best at C2)
                 static const int cb = [] {
                     const char* e = getenv("FFTPIM_CORR_BLOCKS");
-                    return e ? atoi(e) : 2 * 148;
+                    return e ? atoi(e) : 222;
                 }();
                 EvalArgs ac = a;
                 ac.corr_blocks = cb;
