@@ -232,7 +232,7 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
 // weights past the first tap are zero and the indices are clamped, so those
 // taps add exactly 0.
 #ifndef OBS_LPO
-#define OBS_LPO 4
+#define OBS_LPO 2
 #endif
 #ifndef OBS_MINB   // 4 resident blocks: measured faster than 1 (all gathers hoisted, 104 regs)
 #define OBS_MINB 4
