@@ -1093,11 +1093,19 @@ void build(FftpimPlan* P) {
         const int64_t nf = P->n_far;
         if (nf > 3072 || fdims[2] > 32)
             throw Fail{FFTPIM_VALUE, "far grid too large for this build (max 3072 nodes, 32 along z)"};
-        int warps = 8;
-        while (warps > 1 && far_project_smem((int)nf, warps, pr.far_order) > 200 * 1024) --warps;
-        // one wave of one block per SM: the per-block private grids are zeroed and
-        // reduced once per block, so fewer, longer-lived blocks are cheaper
-        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148, (Mown + 32 * warps - 1) / (32 * warps)));
+        static const int warps0 = [] {
+            const char* e = getenv("FFTPIM_FAR_WARPS");
+            return e ? atoi(e) : 8;
+        }();
+        static const int bps = [] {   // blocks per SM
+            const char* e = getenv("FFTPIM_FAR_BPS");
+            return e ? atoi(e) : 1;
+        }();
+        int warps = warps0;
+        while (warps > 1 && far_project_smem((int)nf, warps, pr.far_order) > 200 * 1024 / bps) --warps;
+        // one wave of blocks: the per-block private grids are zeroed and
+        // reduced once per block, so few, long-lived blocks are cheaper
+        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148 * bps, (Mown + 32 * warps - 1) / (32 * warps)));
         P->far_warps = warps;
         P->far_blocks = blocks;
         P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
