@@ -1263,6 +1263,8 @@ static void ensure_batch_buffers(FftpimPlan* P, int64_t batch, int parts) {
     P->bt_E = E;
     if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);   // captured with the old buffers
     P->graph_exec = nullptr;
+    if (P->hgraph_exec) cudaGraphExecDestroy(P->hgraph_exec);
+    P->hgraph_exec = nullptr;
 }
 
 static void evaluate_batched(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s) {
@@ -2196,6 +2198,7 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
             return at.type == cudaMemoryTypeHost;
         };
         FftpimPlan* P = plan;
+        ensure_batch_buffers(P, batch, parts);   // allocations stay outside the capture
         if (P->use_graphs && pinned(q) && pinned(u)) {
             // pinned caller buffers: one graph holds the upload, the evaluation
             // schedule and the download (re-captured when the buffers change)

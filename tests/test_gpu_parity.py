@@ -128,6 +128,10 @@ def test_multi_rhs_batch_matches_single_evaluations(fp, B):
         assert rel_l2(U[b], plan.evaluate(Q[b])) <= 1e-13, b
     Ud = plan.evaluate(torch.from_numpy(Q).cuda()).cpu().numpy()
     assert np.array_equal(U, Ud)
+    q_pin = torch.from_numpy(Q).pin_memory()            # host graph with pinned buffers
+    u_pin = torch.empty(Q.shape, dtype=torch.complex128).pin_memory()
+    plan.native.evaluate(q_pin.numpy(), out=u_pin.numpy())
+    assert np.array_equal(U, u_pin.numpy())
     assert np.array_equal(U, plan.evaluate(Q))          # bitwise reproducible
     g = golden("c2_full.npz")
     Q[3] = q
