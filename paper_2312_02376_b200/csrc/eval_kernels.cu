@@ -230,7 +230,7 @@ __device__ __forceinline__ double2 ld_d2(const cplx* p) {
 }
 
 #ifndef K1E_THREADS
-#define K1E_THREADS 256
+#define K1E_THREADS 128
 #endif
 #ifndef K1_PF
 #define K1_PF 1

@@ -1354,9 +1354,14 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         const bool split = parts == FFTPIM_ALL && P->obs_pre != nullptr;
         // capture order = the order the graph hands ready kernels to the GPU:
         // the near chain (critical path) first, then the far chain, then K4
+        static const int far_gate = [] {   // 1: the far chain starts after K1
+            const char* e = getenv("FFTPIM_FAR_GATE");
+            return e ? atoi(e) : 0;
+        }();
         auto far_chain = [&]() {
             if (!(parts & FFTPIM_FAR)) return;
             CK(cudaStreamWaitEvent(sf, P->ev_fork, 0));
+            if (far_gate && (parts & FFTPIM_NEAR)) CK(cudaStreamWaitEvent(sf, P->ev_k1, 0));
             launch_far_project(a, sf);
             launch_far_sum(a, sf);
             CK(cudaEventRecord(P->ev_join[2], sf));
@@ -1369,7 +1374,7 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
                 const char* e = getenv("FFTPIM_K4_GATE");
                 return e ? atoi(e) : 0;
             }();
-            if (k4_gate == 1) CK(cudaEventRecord(P->ev_k1, sn));
+            if (k4_gate == 1 || far_gate) CK(cudaEventRecord(P->ev_k1, sn));
             if (P->custom_fft) {
                 for (int k = 0; k < 5; ++k) {
                     if (P->stage_on[k]) launch_fft_stage(P->stage[k], sn);
