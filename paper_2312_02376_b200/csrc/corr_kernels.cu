@@ -126,21 +126,26 @@ __device__ __forceinline__ void corr_load(const EvalArgs& a, int64_t t, int lane
 #ifndef CORR_PF
 #define CORR_PF 1
 #endif
-template <bool REAL>
+#ifndef CORR_PF_REAL
+#define CORR_PF_REAL 1
+#endif
+// DEPTH: tiles of pair data in flight beyond the one being reduced (0: none)
+template <bool REAL, int DEPTH>
 __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
     const int64_t stride = (int64_t)gridDim.x * CORR_WARPS;
     int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp;
     const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
-    CorrTile cur;
-    if (CORR_PF && t < T) corr_load<REAL>(a, t, lane, cur);
+    CorrTile cur, n1;
+    if (DEPTH >= 1 && t < T) corr_load<REAL>(a, t, lane, cur);
+    if (DEPTH >= 2 && t + stride < T) corr_load<REAL>(a, t + stride, lane, n1);
     for (; t < T; t += stride) {
         CorrTile nxt;
-        if (CORR_PF) {
-            if (t + stride < T) corr_load<REAL>(a, t + stride, lane, nxt);
-        } else {
+        if (DEPTH == 0) {
             corr_load<REAL>(a, t, lane, cur);
+        } else if (t + DEPTH * stride < T) {
+            corr_load<REAL>(a, t + DEPTH * stride, lane, nxt);
         }
         const int* src = cur.src;
         const double* cr = cur.cr;
@@ -204,7 +209,12 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
         }
         const cplx v = wsum(cplx{accr, acci});
         if (lane == 0) a.seg_val[sbase + seg] = v;
-        if (CORR_PF) cur = nxt;
+        if (DEPTH == 1) {
+            cur = nxt;
+        } else if (DEPTH == 2) {
+            cur = n1;
+            n1 = nxt;
+        }
     }
 }
 
@@ -216,10 +226,11 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.corr_blocks > 0) cap = std::min<int64_t>(cap, a.corr_blocks);
     if (a.corr_blocks < 0) cap = INT32_MAX;   // one block per CORR_WARPS tiles (no grid-stride loop)
     const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, cap);
+    // one tile in flight beyond the one being reduced (measured: deeper is not faster)
     if (a.coef_r)
-        k_corr_tiles<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        k_corr_tiles<true, CORR_PF_REAL><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
     else
-        k_corr_tiles<false><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        k_corr_tiles<false, CORR_PF><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
     fftpim_count_launch();
 }
 
