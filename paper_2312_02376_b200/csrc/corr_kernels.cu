@@ -121,10 +121,108 @@ __device__ __forceinline__ void corr_load(const EvalArgs& a, int64_t t, int lane
     d.sbase = a.seg_base[t];
 }
 
+// segmented accumulation of one tile in pair order: every (row, tile) segment
+// total goes to seg_val[sbase + k]
+__device__ __forceinline__ void corr_reduce_tile(const EvalArgs& a, int lane, const double* cr, const double* ci,
+                                                 const double* qr, const double* qi, unsigned myword, int64_t sbase) {
+    double accr = 0.0, acci = 0.0;
+    int seg = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const double pr = cr[k] * qr[k] - ci[k] * qi[k];
+        const double pi = cr[k] * qi[k] + ci[k] * qr[k];
+        unsigned f = __shfl_sync(0xffffffffu, myword, k);
+        if (k == 0) f &= ~1u;   // a row starting at the tile start is segment 0 itself
+        if (f == 0u) {
+            accr += pr;
+            acci += pi;
+            continue;
+        }
+        // close the open segment with the lanes before the first start
+        int s = __ffs(f) - 1;
+        {
+            double vr = accr + (lane < s ? pr : 0.0), vi = acci + (lane < s ? pi : 0.0);
+            const cplx v = wsum(cplx{vr, vi});
+            if (lane == 0) a.seg_val[sbase + seg] = v;
+            ++seg;
+        }
+        f &= f - 1u;
+        // segments wholly inside this group
+        while (f) {
+            const int s2 = __ffs(f) - 1;
+            const bool in = lane >= s && lane < s2;
+            const cplx v = wsum(cplx{in ? pr : 0.0, in ? pi : 0.0});
+            if (lane == 0) a.seg_val[sbase + seg] = v;
+            ++seg;
+            s = s2;
+            f &= f - 1u;
+        }
+        // the last start opens the new running segment
+        accr = lane >= s ? pr : 0.0;
+        acci = lane >= s ? pi : 0.0;
+    }
+    const cplx v = wsum(cplx{accr, acci});
+    if (lane == 0) a.seg_val[sbase + seg] = v;
+}
+
+// NPSP plans with real charges: a three-stage software pipeline per warp --
+// the stream of tile t + 2s, the 8-byte q gathers of tile t + s (its indices
+// arrived one iteration earlier) and the reduction of tile t overlap, so the
+// gather latency is hidden as well as the stream's.  Same operations in the
+// same order as the generic path (imaginary parts exact zeros): identical bits.
+struct RealTile {
+    int src[8];
+    double cr[8];
+    unsigned word;
+    int64_t sbase;
+};
+
+__device__ __forceinline__ void corr_load_real(const EvalArgs& a, int64_t t, int lane, RealTile& d) {
+    const int64_t T0 = t * CORR_TILE;
+    const int valid = (int)min((int64_t)CORR_TILE, a.n_pairs - T0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int e = 32 * k + lane;
+        const bool ok = e < valid;
+        d.src[k] = ok ? __ldcs(a.pair_src + T0 + e) : 0;
+        d.cr[k] = ok ? __ldcs(a.coef_r + T0 + e) : 0.0;
+    }
+    d.word = lane < 8 ? a.head_bits[(T0 >> 5) + lane] : 0u;
+    d.sbase = a.seg_base[t];
+}
+
+__device__ __forceinline__ void corr_tiles_realq(const EvalArgs& a, int64_t t, int64_t stride, int64_t T, int lane) {
+    const double zero[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    RealTile c0, c1;
+    double q0[8];
+    if (t >= T) return;
+    corr_load_real(a, t, lane, c0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q0[k] = a.q_re[c0.src[k]];
+    if (t + stride < T) corr_load_real(a, t + stride, lane, c1);
+    for (; t < T; t += stride) {
+        RealTile c2;
+        if (t + 2 * stride < T) corr_load_real(a, t + 2 * stride, lane, c2);
+        double q1[8];
+        if (t + stride < T) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q1[k] = a.q_re[c1.src[k]];
+        }
+        corr_reduce_tile(a, lane, c0.cr, zero, q0, zero, c0.word, c0.sbase);
+        c0 = c1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q0[k] = q1[k];
+        c1 = c2;
+    }
+}
+
 // CORR_PF: the next tile's stream loads are issued before this tile's gathers,
 // so every warp keeps two tiles of pair data in flight
 #ifndef CORR_PF
 #define CORR_PF 1
+#endif
+#ifndef CORR_RQ_PIPE   // three-stage pipeline for real coefficients and real charges
+#define CORR_RQ_PIPE 1
 #endif
 #ifndef CORR_PF_REAL
 #define CORR_PF_REAL 1
@@ -137,6 +235,12 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
     const int64_t stride = (int64_t)gridDim.x * CORR_WARPS;
     int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp;
     const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
+#if CORR_RQ_PIPE
+    if (REAL && realq) {
+        corr_tiles_realq(a, t, stride, T, lane);
+        return;
+    }
+#endif
     CorrTile cur, n1;
     if (DEPTH >= 1 && t < T) corr_load<REAL>(a, t, lane, cur);
     if (DEPTH >= 2 && t + stride < T) corr_load<REAL>(a, t + stride, lane, n1);
@@ -170,45 +274,7 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
             qr[k] = qv.re;
             qi[k] = qv.im;
         }
-        // 3. segmented accumulation in pair order
-        double accr = 0.0, acci = 0.0;
-        int seg = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const double pr = cr[k] * qr[k] - ci[k] * qi[k];
-            const double pi = cr[k] * qi[k] + ci[k] * qr[k];
-            unsigned f = __shfl_sync(0xffffffffu, myword, k);
-            if (k == 0) f &= ~1u;   // a row starting at the tile start is segment 0 itself
-            if (f == 0u) {
-                accr += pr;
-                acci += pi;
-                continue;
-            }
-            // close the open segment with the lanes before the first start
-            int s = __ffs(f) - 1;
-            {
-                double vr = accr + (lane < s ? pr : 0.0), vi = acci + (lane < s ? pi : 0.0);
-                const cplx v = wsum(cplx{vr, vi});
-                if (lane == 0) a.seg_val[sbase + seg] = v;
-                ++seg;
-            }
-            f &= f - 1u;
-            // segments wholly inside this group
-            while (f) {
-                const int s2 = __ffs(f) - 1;
-                const bool in = lane >= s && lane < s2;
-                const cplx v = wsum(cplx{in ? pr : 0.0, in ? pi : 0.0});
-                if (lane == 0) a.seg_val[sbase + seg] = v;
-                ++seg;
-                s = s2;
-                f &= f - 1u;
-            }
-            // the last start opens the new running segment
-            accr = lane >= s ? pr : 0.0;
-            acci = lane >= s ? pi : 0.0;
-        }
-        const cplx v = wsum(cplx{accr, acci});
-        if (lane == 0) a.seg_val[sbase + seg] = v;
+        corr_reduce_tile(a, lane, cr, ci, qr, qi, myword, sbase);
         if (DEPTH == 1) {
             cur = nxt;
         } else if (DEPTH == 2) {
