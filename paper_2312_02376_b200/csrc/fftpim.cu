@@ -1678,6 +1678,24 @@ void group_evaluate(GroupImpl* G, const double* q, double* u, cudaStream_t s) {
     CK(cudaGetLastError());
 }
 
+// Orders an evaluation after the plan's previous one when the caller switches
+// streams (same-stream evaluations are already ordered), and serialises the
+// host-side state (graph capture, staging buffers) between threads.
+struct EvalGuard {
+    FftpimPlan* P;
+    cudaStream_t s;
+    std::lock_guard<std::mutex> lock;
+    EvalGuard(FftpimPlan* plan, cudaStream_t stream) : P(plan), s(stream), lock(plan->eval_mu) {
+        if (P->has_last && P->last_stream != s) cudaStreamWaitEvent(s, P->ev_last, 0);
+    }
+    ~EvalGuard() {
+        if (cudaEventRecord(P->ev_last, s) == cudaSuccess) {
+            P->last_stream = s;
+            P->has_last = true;
+        }
+    }
+};
+
 int fail(const Fail& f) {
     g_last_error = f.msg;
     return f.code;
@@ -1741,6 +1759,7 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
         CK(cudaEventCreateWithFlags(&P->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_k1, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_out, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_last, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
         for (auto& e : P->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         P->status = dalloc<DevStatus>(P, 1);
@@ -1841,6 +1860,7 @@ int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* st
     if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
         CK(cudaSetDevice(plan->device));
+        EvalGuard g(plan, (cudaStream_t)stream);
         sweep_evaluate(plan, q, u, (cudaStream_t)stream);
         return FFTPIM_OK;
     } catch (const Fail& f) {
@@ -1856,6 +1876,7 @@ int fftpim_sweep_evaluate_host(FftpimPlan* plan, const double* q, double* u) {
         CK(cudaSetDevice(P->device));
         const int E = P->sw_E;
         cudaStream_t s = P->build_stream, sx = P->aux[2];
+        EvalGuard g(P, s);
         if (P->h_batch < E) {   // persistent device staging (E charge and potential vectors)
             dfree(P, P->h_q);
             dfree(P, P->h_u);
@@ -2169,6 +2190,8 @@ int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t b
     if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});
     if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
+        CK(cudaSetDevice(plan->device));
+        EvalGuard g(plan, (cudaStream_t)stream);
         evaluate(plan, q, u, batch, parts, (cudaStream_t)stream);
         return FFTPIM_OK;
     } catch (const Fail& f) {
@@ -2183,6 +2206,7 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
     try {
         CK(cudaSetDevice(plan->device));
         cudaStream_t s = plan->build_stream;
+        EvalGuard g(plan, s);
         // persistent staging buffers: stable pointers keep the captured graph valid
         if (batch > plan->h_batch) {
             dfree(plan, plan->h_q);
@@ -2257,6 +2281,7 @@ int fftpim_plan_profile(FftpimPlan* plan, const double* q, double* u, int32_t pa
     try {
         CK(cudaSetDevice(plan->device));
         for (auto& e : ev) CK(cudaEventCreate(&e));
+        EvalGuard g(plan, (cudaStream_t)stream);
         evaluate(plan, q, u, 1, parts, (cudaStream_t)stream, ev);
         CK(cudaEventSynchronize(ev[FFTPIM_N_STAGES]));
         for (int k = 0; k < FFTPIM_N_STAGES; ++k) {
@@ -2394,6 +2419,7 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
     if (plan->ev_in) cudaEventDestroy(plan->ev_in);
     if (plan->ev_k1) cudaEventDestroy(plan->ev_k1);
     if (plan->ev_out) cudaEventDestroy(plan->ev_out);
+    if (plan->ev_last) cudaEventDestroy(plan->ev_last);
     if (plan->gstream) cudaStreamDestroy(plan->gstream);
     for (auto e : plan->sw_ready) cudaEventDestroy(e);
     for (auto e : plan->ev_join)

@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <cstdlib>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -218,6 +219,12 @@ struct FftpimPlan {
 
     // batched excitation sweep: E phase shifts differing only
     // along periodic axis sw_axis; one pair list with 2 i_d + 1 phase components
+    // evaluations of one plan share its work buffers: a host mutex plus an
+    // event from the previous evaluation's stream order them across callers
+    std::mutex eval_mu;
+    cudaEvent_t ev_last = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
     bool sweep = false;
     bool near_only = false;            // i_d = 0: eval_near only (no far kernel)
     int sw_axis = 0, sw_E = 0, sw_ncomp = 0;
