@@ -494,6 +494,97 @@ def run_sweep(args):
         dist.destroy_process_group()
 
 
+def run_batch(args):
+    """Multi-RHS: one plan, B charge vectors per step (B >= 8 streams the pairs once
+    per 64 vectors, DESIGN.md 6b').  Row 0 is the config's own charge vector (its
+    parity against the reference is reported), rows 1.. are seeded N(0,1)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2312_02376_b200 as fp
+    from paper_2312_02376_b200 import _native as nat
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch
+    w, pos, q, cfg, box, prm = problem_objects(fp, args.config, e=0)
+    t0 = time.perf_counter()
+    plan = fp.build_plan(cfg, box, fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos), prm, device=local)
+    build_s = time.perf_counter() - t0
+    info = plan.native.info
+    rng = np.random.default_rng(1000 + args.config)
+    Q = rng.standard_normal((B, w.n_points)) + 1j * rng.standard_normal((B, w.n_points))
+    Q[0] = q
+    Q = np.ascontiguousarray(Q)
+    stream = torch.cuda.current_stream()
+    q_dev = torch.from_numpy(Q).to(f"cuda:{local}")
+    u_dev = torch.empty((B, w.n_points), dtype=torch.complex128, device=f"cuda:{local}")
+
+    def step():
+        plan.native.evaluate_into(q_dev.data_ptr(), u_dev.data_ptr(), B, nat.ALL, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = nat.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = (nat.launch_count() - launches0) // args.steps
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    q_pin = torch.from_numpy(Q).pin_memory()
+    u_pin = torch.empty((B, w.n_points), dtype=torch.complex128).pin_memory()
+    for _ in range(2):
+        plan.native.evaluate(q_pin.numpy(), out=u_pin.numpy())
+    te0 = time.perf_counter()
+    n_e2e = max(1, min(args.steps, 5))
+    for _ in range(n_e2e):
+        plan.native.evaluate(q_pin.numpy(), out=u_pin.numpy())
+    te = torch.tensor([(time.perf_counter() - te0) / n_e2e], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    rel, basis = None, None
+    got = u_dev[0].cpu().numpy()
+    for name, key in ((f"c{args.config}_full.npz", None), (f"c{args.config}_subset.npz", "obs_index")):
+        p = os.path.join(REPO, "tests", "golden", name)
+        if os.path.exists(p) and rel is None:
+            g = np.load(p)
+            idx = g[key] if key else slice(None)
+            rel = float(np.linalg.norm(got[idx] - g["u"]) / np.linalg.norm(g["u"]))
+            basis = "row 0, " + ("all observers" if key is None else f"{len(g[key])} seeded observers")
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": world * B * w.n_points / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "complex128/f64",
+            "data": "synthetic (seeded, workloads.py; rows 1.. seeded N(0,1))",
+            "config": {"workload": w.name, "N": w.n_points, "batch": B, "near_grid": list(w.near_grid),
+                       "near_order": w.near_order, "regime": w.regime, "pairs": int(info.n_pairs),
+                       "parallelism": f"replicas x{world}",
+                       "step": f"one evaluate call with {B} charge vectors (multi-RHS)"},
+            "rel_l2_vs_reference": rel, "rel_l2_basis": basis,
+            "e2e": {"value": world * B * w.n_points / float(te.item()), "unit": UNIT,
+                    "h2d_bytes_per_step": 16 * B * w.n_points, "d2h_bytes_per_step": 16 * B * w.n_points},
+            "gpu_launches": int(launches), "build_seconds": build_s, "clocks": clocks.summary(),
+            "cpu_baseline": None}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """Reference algorithm on the host CPU (numpy oracle port; the reference itself
     is Python and is not shipped to the GPU box)."""
@@ -543,6 +634,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true", help="slab-decomposed group (NCCL) even on one GPU")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="multi-RHS: B charge vectors per evaluate call on one plan (C1-C4; C5 uses --per-excitation)")
     ap.add_argument("--per-excitation", action="store_true",
                     help="C5: one ordinary plan per excitation (rank r evaluates excitation r) instead of the sweep")
     args = ap.parse_args()
@@ -552,6 +645,8 @@ def main():
         run_reference(args)
     elif args.slab or (args.config == 4 and int(os.environ.get("WORLD_SIZE", 1)) > 1):
         run_slab(args)
+    elif args.batch > 1:
+        run_batch(args)
     elif args.config == 5 and not args.per_excitation:
         run_sweep(args)
     else:
