@@ -35,7 +35,7 @@ def test_struct_layout_matches_header(tmp_path):
     import subprocess
     if not shutil.which("gcc"):
         pytest.skip("gcc not available")
-    fields = [("FftpimProblem", nat.Problem), ("FftpimInfo", nat.Info)]
+    fields = [("FftpimProblem", nat.Problem), ("FftpimInfo", nat.Info), ("FftpimDirectReport", nat.DirectReport)]
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, cls in fields:
         lines.append(f'printf("%zu\\n", sizeof({cname}));')
