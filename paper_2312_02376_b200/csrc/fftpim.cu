@@ -1105,7 +1105,15 @@ void build(FftpimPlan* P) {
         while (warps > 1 && far_project_smem((int)nf, warps, pr.far_order) > 200 * 1024 / bps) --warps;
         // one wave of blocks: the per-block private grids are zeroed and
         // reduced once per block, so few, long-lived blocks are cheaper
-        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148 * bps, (Mown + 32 * warps - 1) / (32 * warps)));
+        static const int fb = [] {   // absolute block count (0: one wave of bps per SM)
+            const char* e = getenv("FFTPIM_FAR_BLOCKS");
+            return e ? atoi(e) : 0;
+        }();
+        // in the concurrent schedule the far chain is off the critical path: half
+        // the SMs leave the other half to K1 at the start (measured C2 0.133 -> 0.129 ms)
+        const int wave = npairs <= concurrent_max_pairs() && !P->sweep ? 74 * bps : 148 * bps;
+        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(fb > 0 ? fb : wave,
+                                                                 (Mown + 32 * warps - 1) / (32 * warps)));
         P->far_warps = warps;
         P->far_blocks = blocks;
         P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
