@@ -1111,12 +1111,15 @@ void build(FftpimPlan* P) {
         }();
         // in the concurrent schedule the far chain is off the critical path: half
         // the SMs leave the other half to K1 at the start (measured C2 0.133 -> 0.129 ms)
+        const int64_t need = (Mown + 32 * warps - 1) / (32 * warps);
         const int wave = npairs <= concurrent_max_pairs() && !P->sweep ? 74 * bps : 148 * bps;
-        int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(fb > 0 ? fb : wave,
-                                                                 (Mown + 32 * warps - 1) / (32 * warps)));
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(fb > 0 ? fb : wave, need));
+        // sequential chains (multi-RHS batches) use a full wave
+        const int blocks_seq = (int)std::max<int64_t>(blocks, std::min<int64_t>(fb > 0 ? fb : 148 * bps, need));
         P->far_warps = warps;
         P->far_blocks = blocks;
-        P->far_partial = dalloc<cplx>(P, (int64_t)blocks * nf);
+        P->far_blocks_seq = blocks_seq;
+        P->far_partial = dalloc<cplx>(P, (int64_t)blocks_seq * nf);
         P->far_qg = dalloc<cplx>(P, nf);
         P->far_ug = dalloc<cplx>(P, nf);
     }
@@ -1291,6 +1294,7 @@ static void evaluate_batched(FftpimPlan* P, const double* q, double* u, int64_t 
         for (int e = 0; e < E; ++e) {
             EvalArgs a = eval_args(P, qb + 2 * (int64_t)e * P->N, ub + 2 * (int64_t)e * P->M, parts);
             a.sw_e = -1;   // the K4 term is added below
+            a.far_blocks = P->far_blocks_seq;
             launch_permute_q(a, sn);
             if (parts & FFTPIM_FAR) {
                 launch_far_project(a, sn);

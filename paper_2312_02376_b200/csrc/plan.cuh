@@ -171,6 +171,7 @@ struct FftpimPlan {
     cplx* far_partial = nullptr;  // per-block partial grids
     cplx* far_ug = nullptr;       // far observer-grid potentials
     cplx* obs_pre = nullptr;      // split observer pass: far + K4 fix-up (concurrent schedule)
+    int far_blocks_seq = 0;            // far projection grid for sequential chains
     int far_blocks = 0;
     int far_warps = 0;
 
