@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
     const int t = ZC ? threadIdx.x % T : threadIdx.x / CPB;
     const int col = blockIdx.x * CPB + c;
     const bool okc = col < st.nb0;
-    if (st.spec && st.spec_s0 == 1) {
+    if (st.spec && st.spec_s0 == 1 && !(st.fold_y | st.fold_z)) {
         // pull this block's spectrum rows (CPB consecutive columns per k) into L2
         // now; they are read after the forward transform
         const int ncols = min(CPB, st.nb0 - (int)blockIdx.x * CPB);
@@ -483,7 +483,14 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
     cplx* out = st.out + (int64_t)blockIdx.y * st.out_s1 + (int64_t)col * st.out_s0;
     if (st.spec) {
         reg_fwd<L, -1>(a, buf, t, st.tw);
-        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + (int64_t)col * st.spec_s0;
+        int64_t fcol = col;
+        if (st.fold_y | st.fold_z) {
+            int ky = col / st.spec_L2, kz = col - ky * st.spec_L2;
+            if (st.fold_y && 2 * ky > st.fold_y) ky = st.fold_y - ky;
+            if (st.fold_z && 2 * kz > st.fold_z) kz = st.fold_z - kz;
+            fcol = (int64_t)ky * st.spec_L2 + kz;
+        }
+        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + fcol * st.spec_s0;
         if (okc) {
 #pragma unroll
             for (int s = 0; s < E / T; ++s)

@@ -328,6 +328,18 @@ void setup_fft_pipeline(FftpimPlan* P, const int dims[3], cudaStream_t s) {
         st.nb0 = (int)L12; st.in_s0 = 1; st.out_s0 = 1;
         st.nb1 = 1; st.in_s1 = 0; st.out_s1 = 0;
         st.spec = P->khat; st.spec_stride = L12; st.spec_s0 = 1; st.spec_s1 = 0;
+        {
+            const FftpimProblem& pr = P->prob;
+            const char* e = getenv("FFTPIM_KHAT_FOLD");
+            const bool on = !(e && e[0] == '0');
+            auto even = [&](int a) {
+                if (!on || dims[a] == 1 || (P->sweep && a == P->sw_axis)) return false;
+                return a >= pr.dim || (pr.kshift[a][0] == 0.0 && pr.kshift[a][1] == 0.0);
+            };
+            st.fold_y = even(1) ? L[1] : 0;
+            st.fold_z = even(2) ? L[2] : 0;
+            st.spec_L2 = L[2];
+        }
         P->stage[2] = st;
         P->stage_on[2] = true;
     }
@@ -379,6 +391,7 @@ void setup_fft_pipeline_shard(FftpimPlan* P, const int dims[3], cudaStream_t s) 
     st[2].in = P->a2a_recv; st[2].out = P->a2a_recv; st[2].lin = n0; st[2].lout = n0;
     st[2].in_stride = ncol; st[2].out_stride = ncol; st[2].nb0 = (int)ncol; st[2].in_s0 = 1; st[2].out_s0 = 1;
     st[2].spec = P->khat; st[2].spec_stride = ncol; st[2].spec_s0 = 1;
+    st[2].fold_y = st[2].fold_z = 0;   // a column slice of khat: no symmetric folding
     st[2].B = std::max(1, std::min(st[2].nb0, fft_block_elems() / st[2].L));
     // S4: y inverse, B -> A
     st[3].in = P->fbufB; st[3].out = P->fbufA; st[3].nb1 = nl;

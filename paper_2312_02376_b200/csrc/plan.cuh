@@ -84,6 +84,11 @@ struct FftStage {
     int sign;                   // -1 forward, +1 inverse (ignored when spec is set)
     const cplx* spec;           // fused x stage: forward, multiply by spec, inverse
     int64_t spec_stride, spec_s0, spec_s1;
+    // khat even along y / z (non-periodic axis, or periodic without phase
+    // shift): the fused register stage reads column (ky, kz) at its folded
+    // index, so only a quarter / half of the spectrum is touched and it stays
+    // L2-resident (0 = no fold, else the axis length); spec_L2 = 2 n2
+    int fold_y, fold_z, spec_L2;
     const cplx* tw;             // exp(-2 pi i t / L), t < L
     const cplx* twp;            // per-pass compact twiddles, pass order
     int ntwp;
