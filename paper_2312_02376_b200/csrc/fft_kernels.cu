@@ -592,7 +592,14 @@ __global__ void __launch_bounds__(RF3_THREADS) k_fft_reg3(FftStage st) {
     if (st.spec) {
         reg3_split<M, -1>(a, in, st.in_stride, st.lin, okc, r, t, st.tw);
         reg_fwd<M, -1, 3>(a, buf, t, st.tw);
-        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + (int64_t)col * st.spec_s0;
+        int64_t fcol = col;
+        if (st.fold_y | st.fold_z) {   // even khat along y / z: read the folded column
+            int ky = col / st.spec_L2, kz = col - ky * st.spec_L2;
+            if (st.fold_y && 2 * ky > st.fold_y) ky = st.fold_y - ky;
+            if (st.fold_z && 2 * kz > st.fold_z) kz = st.fold_z - kz;
+            fcol = (int64_t)ky * st.spec_L2 + kz;
+        }
+        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + fcol * st.spec_s0;
         if (okc) {
 #pragma unroll
             for (int s2 = 0; s2 < E / T; ++s2)
