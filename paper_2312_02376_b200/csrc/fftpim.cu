@@ -1334,6 +1334,14 @@ static void evaluate_batched(FftpimPlan* P, const double* q, double* u, int64_t 
     CK(cudaGetLastError());
 }
 
+static bool far_side() {
+    static const bool on = [] {
+        const char* e = getenv("FFTPIM_FAR_SIDE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s) {
     if (batched_k4(P, batch, parts) && P->bt_E > 0) {
         evaluate_batched(P, q, u, batch, parts, s);
@@ -1345,7 +1353,15 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         for (int64_t b = 0; b < batch; ++b) {
             EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
             launch_permute_q(a, s);
-            if (parts & FFTPIM_FAR) {
+            // the latency-bound far chain overlaps K1 and the FFT stages on a side stream
+            const bool side = (parts & FFTPIM_FAR) && (parts & FFTPIM_NEAR) && far_side();
+            if (side) {
+                CK(cudaEventRecord(P->ev_fork, s));
+                CK(cudaStreamWaitEvent(P->aux[2], P->ev_fork, 0));
+                launch_far_project(a, P->aux[2]);
+                launch_far_sum(a, P->aux[2]);
+                CK(cudaEventRecord(P->ev_join[2], P->aux[2]));
+            } else if (parts & FFTPIM_FAR) {
                 launch_far_project(a, s);
                 launch_far_sum(a, s);
             }
@@ -1362,6 +1378,7 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
                 }
                 launch_corr_tiles(a, s);
             }
+            if (side) CK(cudaStreamWaitEvent(s, P->ev_join[2], 0));
             launch_observers(a, s);
         }
         CK(cudaGetLastError());
