@@ -232,10 +232,13 @@ __device__ __forceinline__ double2 ld_d2(const cplx* p) {
 #ifndef K1E_THREADS
 #define K1E_THREADS 128
 #endif
+#ifndef K1E_MINB
+#define K1E_MINB 8
+#endif
 #ifndef K1_PF
 #define K1_PF 1
 #endif
-__global__ void __launch_bounds__(K1E_THREADS, 1) k_k1_spmv(EvalArgs a) {
+__global__ void __launch_bounds__(K1E_THREADS, K1E_MINB) k_k1_spmv(EvalArgs a) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int n1 = a.g.n[1], n2 = a.g.n[2];
     if (t >= (int64_t)a.knx * n1 * n2) return;
