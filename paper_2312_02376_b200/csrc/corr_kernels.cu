@@ -468,11 +468,13 @@ static void launch_observers_lpo(const EvalArgs& a, cudaStream_t s, int mode) {
     }
 }
 
-// lanes per observer: 4 for small observer sets (more threads in flight), 2
-// otherwise (measured: C2 / C5 observer pass 10-30 % faster than 4 lanes)
+// lanes per observer: 4 for small observer sets (more threads in flight) and
+// order >= 4, 2 otherwise (measured: C2 / C5 observer pass 10-30 % faster)
 void launch_observers(const EvalArgs& a, cudaStream_t s, int mode) {
     if (a.M == 0) return;
-    if (a.M <= OBS_SMALL_M)
+    // 5-tap (order 4) stencils: 13 entries per lane at 2 lanes spill under the
+    // 64-register budget, so those keep 4 lanes
+    if (a.M <= OBS_SMALL_M || a.g.order >= 4)
         launch_observers_lpo<4>(a, s, mode);
     else
         launch_observers_lpo<2>(a, s, mode);
