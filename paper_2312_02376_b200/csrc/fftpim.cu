@@ -1044,6 +1044,13 @@ void build(FftpimPlan* P) {
                 CK(cudaMemsetAsync(P->k1_idx, 0, sizeof(int) * total, s));
                 CK(cudaMemsetAsync(P->k1_wgt, 0, sizeof(double) * total, s));
                 launch_k1_fill(a, row_of, off, P->k1_orig ? P->src_perm : nullptr, P->k1_idx, P->k1_wgt, s);
+                if (P->k1_orig && getenv("FFTPIM_K1_ONE_ORDER") == nullptr) {
+                    // second index array in sorted order for device-resident charges
+                    // (same rows, same weights: the fill rewrites identical values)
+                    P->k1_idx_sorted = dalloc<int>(P, total);
+                    CK(cudaMemsetAsync(P->k1_idx_sorted, 0, sizeof(int) * total, s));
+                    launch_k1_fill(a, row_of, off, nullptr, P->k1_idx_sorted, P->k1_wgt, s);
+                }
                 P->k1_cnt = cnt;
                 P->k1_row = row_of;
                 P->k1_off = off;
@@ -1108,7 +1115,8 @@ void build(FftpimPlan* P) {
             throw Fail{FFTPIM_VALUE, "far grid too large for this build (max 3072 nodes, 32 along z)"};
         static const int warps0 = [] {
             const char* e = getenv("FFTPIM_FAR_WARPS");
-            return e ? atoi(e) : 8;
+            // k_far_project is __launch_bounds__(256): at most 8 warps
+            return e ? std::min(std::max(atoi(e), 1), 8) : 8;
         }();
         static const int bps = [] {   // blocks per SM
             const char* e = getenv("FFTPIM_FAR_BPS");
@@ -1149,6 +1157,14 @@ void build(FftpimPlan* P) {
     }
     P->info.n_src = N;
     P->info.n_obs = M;
+}
+
+// K1 reads the caller-order charges (starting alongside the permutation) only in
+// the host entry's graph: with device-resident charges the sorted-order operator
+// is faster (C2 122.6 -> 119.7 us), with the upload in the graph the caller-order
+// one is (e2e 3.2e8 -> 3.4e8 points/s); both operators sum in the same order
+static bool k1_caller_order(const FftpimPlan* P) {
+    return P->k1_orig && (P->host_call || P->k1_idx_sorted == nullptr);
 }
 
 EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
@@ -1215,8 +1231,8 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.k1_cnt = P->k1_cnt;
     a.k1_row = P->k1_row;
     a.k1_off = P->k1_off;
-    a.k1_q = P->k1_orig ? a.q : P->q_sorted;
-    a.k1_idx = P->k1_idx;
+    a.k1_q = k1_caller_order(P) ? a.q : P->q_sorted;
+    a.k1_idx = P->k1_orig && !k1_caller_order(P) ? P->k1_idx_sorted : P->k1_idx;
     a.k1_wgt = P->k1_wgt;
     a.kx0 = 0;
     a.knx = P->near_g.n[0];
@@ -1387,7 +1403,7 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
     for (int64_t b = 0; b < batch; ++b) {
         EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
         // a K1 reading the caller-order charges starts alongside the permutation
-        if (P->k1_orig) CK(cudaEventRecord(P->ev_start, s));
+        if (k1_caller_order(P)) CK(cudaEventRecord(P->ev_start, s));
         launch_permute_q(a, s);
         CK(cudaEventRecord(P->ev_fork, s));
         cudaStream_t sn = P->aux[0], sc = P->aux[1], sf = P->aux[2];
@@ -1410,7 +1426,7 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         };
         if (!(parts & FFTPIM_NEAR)) far_chain();
         if (parts & FFTPIM_NEAR) {
-            CK(cudaStreamWaitEvent(sn, P->k1_orig ? P->ev_start : P->ev_fork, 0));
+            CK(cudaStreamWaitEvent(sn, k1_caller_order(P) ? P->ev_start : P->ev_fork, 0));
             launch_near_project(a, sn);
             static const int k4_gate = [] {   // 1: K4 starts after K1, 2: after the forward FFT stages
                 const char* e = getenv("FFTPIM_K4_GATE");
@@ -2284,11 +2300,14 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
                 const long long l0 = g_launches.load();
                 try {
                     CK(cudaMemcpyAsync(P->h_q, q, qb, cudaMemcpyHostToDevice, s));
+                    P->host_call = true;   // K1 reads the uploaded caller-order charges
                     evaluate_schedule(P, P->h_q, P->h_u, batch, parts, s);
+                    P->host_call = false;
                     CK(cudaMemcpyAsync(u, P->h_u, ub, cudaMemcpyDeviceToHost, s));
                     P->hkernels_per_eval = (int)((g_launches.load() - l0) / batch);
                 } catch (...) {
                     P->capturing = false;
+                    P->host_call = false;
                     cudaStreamEndCapture(s, &graph);
                     if (graph) cudaGraphDestroy(graph);
                     throw;

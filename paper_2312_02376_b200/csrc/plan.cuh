@@ -144,6 +144,8 @@ struct FftpimPlan {
     int64_t* k1_off = nullptr;    // (slices + 1) entry offsets
     bool k1_orig = false;         // entries index the caller-order charges
     int* k1_idx = nullptr;
+    int* k1_idx_sorted = nullptr;  // k1_orig plans: the same operator indexing q_sorted
+    bool host_call = false;       // capturing the host entry's graph (upload inside)
     double* k1_wgt = nullptr;
     int64_t k1_slots = 0;
 

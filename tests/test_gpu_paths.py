@@ -81,6 +81,8 @@ def test_host_entries_and_alignment():
     for _ in range(3):   # capture, then replays
         nplan.evaluate(q_pin.numpy(), out=u_pin.numpy())
     u_dev = nplan.evaluate(torch.from_numpy(q).cuda()).cpu().numpy()
+    # the pinned host graph's K1 indexes the caller-order charges, the device
+    # path's the sorted ones: same rows, same summation order -> bitwise equal
     np.testing.assert_array_equal(u_pin.numpy(), u_page)
     np.testing.assert_array_equal(u_dev, u_page)
     # a new pinned output buffer re-captures the host graph
