@@ -4,15 +4,18 @@ points/sec per evaluation, HBM-roofline fraction, relative L2 error).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
 
 A step is one SolvePlan.evaluate (solver.py:24-25) of the config's charge
-vector, inputs resident in HBM.  Default workload: configs[1] = C2 (1D-periodic
-Helmholtz, N = 65,536, 64^3 grid, order 3) -- the BASELINE config that fits
-one GPU and that the reference itself can run.  C1/C2/C3 shard as replicas
-(SURVEY.md 8e): under torchrun each rank evaluates its own replica, value =
-total points of all ranks / max-over-ranks time ("scaling": "weak").
+vector, inputs resident in HBM.  Default workload: configs[3] = C4 (3D-periodic
+Helmholtz with phase shift, N = 8,388,608, 256^3 grid, order 4) -- the largest
+BASELINE config that fits one B200 (122 GB of correction pairs).  At N > 1 C4 is
+slab-decomposed over the ranks (NCCL all-to-all FFT transposes, "scaling":
+"strong"); C5 shards its 64 excitations; C1/C2/C3 run replicas ("weak").
+`--gpus N` without torchrun re-launches itself under torch.distributed.run.
 
 `--impl reference` times the reference algorithm on the host CPU (the numpy
-oracle port; the reference is pure Python/numpy): plan built once by the
-oracle (multi-process), then single-threaded numpy evaluations.
+oracle port; the reference is pure Python/numpy): C1/C2 a full evaluation of the
+oracle plan per step; C3/C4/C5 (plans of 35-221 GB that no host builds in
+minutes) the composed time of SURVEY.md 8d per step (oracle/composed.py: every
+eval stage timed on a bounded sample and scaled to the full size).
 """
 from __future__ import annotations
 
@@ -115,7 +118,8 @@ def stage_bytes(w, info, n_far):
     return {
         "permute_q": 16 * N + 4 * N + 16 * N,
         "far_project": N * (24 + 16) + 16 * n_far,
-        "near_project": N * (24 + 16) + 16 * nfft,       # padded grid written once (zeros included)
+        # positions + q read, the n^3 grid written once (the pruned FFT never stores the padding)
+        "near_project": N * (24 + 16) + 16 * ng,
         "fft_forward": 2 * 16 * nfft,
         "spectrum_mul": 3 * 16 * nfft,
         "fft_inverse": 2 * 16 * nfft,
@@ -124,6 +128,36 @@ def stage_bytes(w, info, n_far):
         # K3 + K5c + fix-up: observer stencil, grid reads, row sums, u written once
         "observers": M * 24 + 16 * ng + 8 * M + 16 * M + 16 * M,
     }
+
+
+def workload_config(w) -> dict:
+    """The `config` dict both arms print (identical keys and values)."""
+    cfg = {"workload": w.name, "N": w.n_points, "near_grid": list(w.near_grid), "near_order": w.near_order,
+           "regime": w.regime,
+           "l2": "inputs larger than L2 (no flush): the correction-pair stream alone is "
+                 "0.23 GB (C2) to 122 GB (C4) per evaluation"}
+    if w.excitations > 1:
+        cfg["excitations"] = w.excitations
+    return cfg
+
+
+def oracle_problem(w, e=0):
+    from oracle.problem import make_problem
+    kshift = c5_kshift(e) if w.excitations > 1 else w.kshift
+    return make_problem(w.dim, L=w.L, D=w.D, k0=w.k0, kshift=kshift, regime=w.regime, **w.params())
+
+
+def composed_cpu_baseline(w, pos, q, n_pairs=None, reps=3):
+    """SURVEY.md 8d composed CPU time of one full evaluation (oracle/composed.py):
+    the oracle's numpy eval stages timed on a bounded sample and scaled; best of
+    `reps` (cli.py:360-366)."""
+    from oracle.composed import ComposedSampler
+    s = ComposedSampler(oracle_problem(w), pos, q, n_pairs=n_pairs)
+    runs = [s.measure() for _ in range(reps)]
+    best, stages = min(runs, key=lambda r: r[0])
+    return {"value": w.n_points / best, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": s.describe() + f"; best of {reps}; host nproc={os.cpu_count()}",
+            "seconds_per_eval": best, "stages_s": stages, "setup_seconds": s.setup_seconds}
 
 
 def cpu_baseline_from_plan(w, plan, pos, q, budget_s=20.0):
@@ -266,21 +300,20 @@ def run_b200(args):
         rel_basis = f"{len(idx)} seeded observers (reference subset run)"
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and int(info.n_pairs) < 10**9:
-        cpu, u_cpu = cpu_baseline_from_plan(w, plan, pos, q)
-        if rel is None:
-            rel = float(np.linalg.norm(u_dev.cpu().numpy() - u_cpu) / np.linalg.norm(u_cpu))
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if int(info.n_pairs) < 10**8:     # C1/C2: full oracle evaluations
+            cpu, u_cpu = cpu_baseline_from_plan(w, plan, pos, q)
+            if rel is None:
+                rel = float(np.linalg.norm(u_dev.cpu().numpy() - u_cpu) / np.linalg.norm(u_cpu))
+        else:                             # C3/C4/C5: composed
+            cpu = composed_cpu_baseline(w, pos, q, n_pairs=int(info.n_pairs))
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "complex128/f64", "data": "synthetic (seeded, workloads.py)",
-            "config": {"workload": w.name, "N": w.n_points, "near_grid": list(w.near_grid),
-                       "near_order": w.near_order, "regime": w.regime, "pairs": int(info.n_pairs),
-                       "parallelism": f"replicas x{world}",
-                       "l2": "working set > L2 (correction stream alone "
-                             f"{int(info.n_pairs) * (12 if info.real_coefficients else 20) / 1e6:.0f} MB)"},
+            "config": workload_config(w), "pairs": int(info.n_pairs), "parallelism": f"replicas x{world}",
             "rel_l2_vs_reference": rel, "rel_l2_basis": rel_basis,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
@@ -350,8 +383,29 @@ def run_slab(args):
             dist.barrier()
     launches = (nat.launch_count() - launches0) // args.steps
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=f"cuda:{local}")
+    # e2e: every rank uploads the (replicated) charges from pinned host memory,
+    # evaluates its slab and downloads the potential buffer (its own observers)
+    q_pin = torch.from_numpy(q).pin_memory()
+    u_pin = torch.empty(w.n_points, dtype=torch.complex128).pin_memory()
+    q_e2e = torch.empty_like(q_dev)
+    u_e2e = torch.zeros_like(u_dev)
+
+    def e2e_step():
+        q_e2e.copy_(q_pin, non_blocking=True)
+        grp.evaluate_into(q_e2e.data_ptr(), u_e2e.data_ptr(), stream.cuda_stream)
+        u_pin.copy_(u_e2e, non_blocking=True)
+        stream.synchronize()
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    te0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    te = torch.tensor([(time.perf_counter() - te0) / args.steps], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
         dist.all_reduce(u_dev)   # each rank holds only its own observers
     ms = float(t.item())
     rel, basis = None, None
@@ -371,14 +425,14 @@ def run_slab(args):
             "metric": METRIC, "value": w.n_points / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "complex128/f64", "data": "synthetic (seeded, workloads.py)",
-            "config": {"workload": w.name, "N": w.n_points, "near_grid": list(w.near_grid), "near_order": w.near_order,
-                       "regime": w.regime, "pairs": P, "parallelism": f"slab x{world} (NCCL all-to-all)",
-                       "l2": "working set > L2"},
+            "config": workload_config(w), "pairs": P, "parallelism": f"slab x{world} (NCCL all-to-all)",
             "rel_l2_vs_reference": rel, "rel_l2_basis": basis,
             "roofline": {"bound": "hbm", "kernel": "whole evaluation (correction stream dominated)",
                          "achieved": P * 20 / (ms * 1e-3) / 1e9 / world, "peak": peak, "unit": "GB/s",
                          "frac": P * 20 / (ms * 1e-3) / 1e9 / world / peak, "peak_kind": peak_kind, "traffic": None},
-            "e2e": None, "gpu_launches": int(launches), "build_seconds": build_s, "clocks": clocks.summary(),
+            "e2e": {"value": w.n_points / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": 16 * w.n_points,
+                    "d2h_bytes_per_step": 16 * w.n_points},
+            "gpu_launches": int(launches), "build_seconds": build_s, "clocks": clocks.summary(),
             "cpu_baseline": None}))
     if world > 1:
         dist.barrier()
@@ -453,6 +507,10 @@ def run_sweep(args):
                       device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = composed_cpu_baseline(w, pos, qall[es[0]], n_pairs=int(sw.info.n_pairs))
+        cpu["sample"] = "per excitation (the sweep's unit): " + cpu["sample"]
     rel, basis = None, None
     spath = os.path.join(REPO, "tests", "golden", f"c{args.config}_subset.npz")
     if rank == 0 and os.path.exists(spath):
@@ -472,11 +530,10 @@ def run_sweep(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "complex128/f64",
             "data": "synthetic (seeded, workloads.py)",
-            "config": {"workload": w.name, "N": w.n_points, "excitations": E, "near_grid": list(w.near_grid),
-                       "near_order": w.near_order, "regime": w.regime, "pairs": P,
-                       "parallelism": f"excitation shards x{world} (sweep plans: phase-factorised pairs)",
-                       "step": f"one sweep evaluation of {len(es)} excitations per rank",
-                       "l2": f"working set > L2 (coefficient components {P * 16 * nc / 1e9:.0f} GB)"},
+            "config": workload_config(w), "pairs": P,
+            "parallelism": f"excitation shards x{world} (sweep plans: phase-factorised pairs)",
+            "step": f"one sweep evaluation of {len(es)} excitations per rank "
+                    f"(coefficient components {P * 16 * nc / 1e9:.0f} GB streamed)",
             "rel_l2_vs_reference": rel, "rel_l2_basis": basis,
             "roofline": {"bound": "hbm", "kernel": "corr_sweep (batched precorrection)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
@@ -488,7 +545,7 @@ def run_sweep(args):
             "e2e": {"value": E * w.n_points / float(te.item()), "unit": UNIT,
                     "h2d_bytes_per_step": 16 * w.n_points * len(es), "d2h_bytes_per_step": 16 * w.n_points * len(es)},
             "gpu_launches": int(launches), "build_seconds": build_s, "clocks": clocks.summary(),
-            "cpu_baseline": None}))
+            "cpu_baseline": cpu}))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -571,10 +628,8 @@ def run_batch(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "complex128/f64",
             "data": "synthetic (seeded, workloads.py; rows 1.. seeded N(0,1))",
-            "config": {"workload": w.name, "N": w.n_points, "batch": B, "near_grid": list(w.near_grid),
-                       "near_order": w.near_order, "regime": w.regime, "pairs": int(info.n_pairs),
-                       "parallelism": f"replicas x{world}",
-                       "step": f"one evaluate call with {B} charge vectors (multi-RHS)"},
+            "config": dict(workload_config(w), batch=B), "pairs": int(info.n_pairs),
+            "parallelism": f"replicas x{world}", "step": f"one evaluate call with {B} charge vectors (multi-RHS)",
             "rel_l2_vs_reference": rel, "rel_l2_basis": basis,
             "e2e": {"value": world * B * w.n_points / float(te.item()), "unit": UNIT,
                     "h2d_bytes_per_step": 16 * B * w.n_points, "d2h_bytes_per_step": 16 * B * w.n_points},
@@ -585,44 +640,85 @@ def run_batch(args):
         dist.destroy_process_group()
 
 
+def arm_scaling(config: int, world: int) -> str:
+    """C4 at N > 1 is one partitioned problem (slabs) and C5 shards one fixed sweep:
+    total work fixed ("strong"); replicas otherwise ("weak")."""
+    return "strong" if (config == 4 and world > 1) or config == 5 else "weak"
+
+
 def run_reference(args):
     """Reference algorithm on the host CPU (numpy oracle port; the reference itself
-    is Python and is not shipped to the GPU box)."""
+    is Python and is not shipped to the GPU box).  Rank 0 alone runs; other ranks
+    exit without work.  C1/C2: each step one full evaluation of the oracle plan
+    (built once, multi-process).  C3/C4/C5: each step one composed evaluation
+    (oracle/composed.py); C5 counts its 64 excitations per step, each
+    costing one per-excitation evaluation (same geometry and pair count)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle.parallel import build_plan_parallel
-    from oracle.problem import make_problem
     w = CONFIGS[args.config]
     pos, q = make_inputs(args.config)
-    pb = make_problem(w.dim, L=w.L, D=w.D, k0=w.k0, kshift=w.kshift, regime=w.regime, **w.params())
-    t0 = time.perf_counter()
-    plan = build_plan_parallel(pb, pos)
-    build_s = time.perf_counter() - t0
-    for _ in range(args.warmup):
-        plan.evaluate(q)
-    times = []
-    for _ in range(args.steps):
+    if w.excitations > 1:
+        q = q[0]
+    extra = {}
+    if args.config in (1, 2):
+        from oracle.parallel import build_plan_parallel
         t0 = time.perf_counter()
-        plan.evaluate(q)
-        times.append(time.perf_counter() - t0)
+        plan = build_plan_parallel(oracle_problem(w), pos)
+        build_s = time.perf_counter() - t0
+        for _ in range(args.warmup):
+            plan.evaluate(q)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            plan.evaluate(q)
+            times.append(time.perf_counter() - t0)
+        sample = (f"each step = one full {w.name} evaluation by the numpy oracle (reference algorithm; its eval "
+                  f"loops are single-threaded numpy); plan built once by the oracle over {os.cpu_count()} "
+                  f"processes in {build_s:.1f} s")
+        extra["pairs"] = int(plan.near.pair_obs.size)
+    else:
+        from oracle.composed import ComposedSampler
+        t0 = time.perf_counter()
+        s = ComposedSampler(oracle_problem(w), pos, q)
+        build_s = time.perf_counter() - t0
+        for _ in range(args.warmup):
+            s.measure()
+        times, stages = [], []
+        for _ in range(args.steps):
+            sec, st = s.measure()
+            times.append(sec * w.excitations)
+            stages.append(st)
+        sample = (f"each step = " + (f"{w.excitations} x " if w.excitations > 1 else "") +
+                  "one " + s.describe() + f"; sampled operands prepared once in {build_s:.1f} s")
+        extra["pairs_estimated"] = s.P
+        extra["stages_s_median"] = {k: float(np.median([x[k] for x in stages])) for k in stages[0]}
     sec = float(np.median(times))
-    value = w.n_points / sec
+    value = w.excitations * w.n_points / sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "complex128/f64",
+        "scaling": arm_scaling(args.config, world), "vs_baseline": None, "dtype": "complex128/f64",
         "data": "synthetic (seeded, workloads.py)",
-        "config": {"workload": w.name, "N": w.n_points, "near_grid": list(w.near_grid),
-                   "near_order": w.near_order, "regime": w.regime, "pairs": int(plan.near.pair_obs.size)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"each step = one full {w.name} evaluation by the numpy oracle "
-                                   f"(reference algorithm; its eval loops are single-threaded numpy); plan "
-                                   f"built once by the oracle over {os.cpu_count()} processes in {build_s:.1f} s"},
+        "config": workload_config(w),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "build_seconds": build_s,
     }
+    line.update(extra)
     print(json.dumps(line))
+
+
+def relaunch_distributed(args) -> int:
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run with
+    N ranks on this node (the driver's own launch line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -633,7 +729,7 @@ def main():
     # first-replay effects); everything else 20 after 5
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true", help="slab-decomposed group (NCCL) even on one GPU")
@@ -642,6 +738,8 @@ def main():
     ap.add_argument("--per-excitation", action="store_true",
                     help="C5: one ordinary plan per excitation (rank r evaluates excitation r) instead of the sweep")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     short = args.impl == "b200" and args.config in (1, 2) and args.batch == 1 and not args.slab
     if args.steps is None:
         args.steps = 200 if short else 20
