@@ -322,6 +322,8 @@ __global__ void __launch_bounds__(K1E_THREADS, K1E_MINB) k_k1_spmv(EvalArgs a) {
 }
 
 void launch_near_project(const EvalArgs& a, cudaStream_t s) {
+    if (a.k1_rec && launch_k1_lines_g(a, a.k1_rec, s)) return;
+    if (a.k1_pos && launch_k1_lines(a, a.k1_pos, s)) return;
     if (a.k1_off) {
         k_k1_spmv<<<nblk((int64_t)a.knx * a.g.n[1] * a.g.n[2], K1E_THREADS), K1E_THREADS, 0, s>>>(a);
         fftpim_count_launch();

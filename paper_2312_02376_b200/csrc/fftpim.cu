@@ -633,6 +633,22 @@ void build(FftpimPlan* P) {
     P->src_w = dalloc<double>(P, N * 3 * W);
     P->src_start = dalloc<int>(P, N * 3);
     launch_stencils(d_src, P->src_perm, N, P->near_g, P->src_w, P->src_start, P->status, 20, s);
+    {
+        // K1: line sweep (stencils from sorted positions) by default for large
+        // point sets, the plan-time sliced-ELL operator otherwise;
+        // FFTPIM_K1=lines|ell|gather|taps overrides
+        const char* e = getenv("FFTPIM_K1");
+        const bool ok = W >= 3 && W <= 6;
+        const std::string mode = e ? e : "ell";
+        P->k1_lines = ok && (mode == "lines" || mode == "lines_smem");
+        if (P->k1_lines && mode == "lines_smem") {
+            P->src_pos_s = dalloc<double>(P, 3 * N);
+            launch_gather_pos(d_src, P->src_perm, N, P->src_pos_s, s);
+        } else if (P->k1_lines) {
+            P->src_rec = dalloc<double>(P, N * stencil_record_width(W));
+            launch_stencil_records(P->src_w, P->src_start, N, W, P->src_rec, s);
+        }
+    }
     P->src_fw = dalloc<double>(P, N * 3 * WF);
     P->src_fstart = dalloc<int>(P, N * 3);
     launch_stencils(d_src, P->src_perm, N, P->far_sg, P->src_fw, P->src_fstart, P->status, 21, s);
@@ -651,6 +667,20 @@ void build(FftpimPlan* P) {
     P->obs_fstart = dalloc<int>(P, M * 3);
     launch_stencils(d_obs, P->obs_perm, M, P->far_og, P->obs_fw, P->obs_fstart, P->status, 23, s);
     check_status(P, "stencil construction");
+    {
+        // observer pass with stencils from sorted positions (line_kernels.cu) for
+        // large observer sets; FFTPIM_OBS=pos|weights overrides
+        const char* e = getenv("FFTPIM_OBS");
+        P->obs_pos_pass = W >= 3 && W <= 6 && WF >= 3 && WF <= 5 && (e ? std::string(e) == "pos" : false);
+        if (P->obs_pos_pass) {
+            if (same && P->src_pos_s) {
+                P->obs_pos_s = P->src_pos_s;
+            } else {
+                P->obs_pos_s = dalloc<double>(P, 3 * M);
+                launch_gather_pos(d_obs, P->obs_perm, M, P->obs_pos_s, s);
+            }
+        }
+    }
 
     // ---- slab ownership: planes [X0, X1), observers/sources whose
     // near stencil starts there = one contiguous range of the x-major sorted order
@@ -711,7 +741,7 @@ void build(FftpimPlan* P) {
         // grids keep the gather K1.  FFTPIM_K1=taps|gather overrides.
         const char* e = getenv("FFTPIM_K1");
         const double density = (double)N / (double)prod3(P->near_g.nc);
-        bool taps = density >= 1.0;
+        bool taps = density >= 1.0 && !P->k1_lines;
         if (e) taps = std::string(e) == "taps";
         if (taps && dims[0] > 1 && dims[1] > 1 && dims[2] > 1 && pr.near_order >= 2 && pr.near_order <= 4)
             P->k1_scratch = dalloc<cplx>(P, k1_scratch_elems(P->near_g, P->n0_loc));
@@ -992,7 +1022,7 @@ void build(FftpimPlan* P) {
     // half the free memory; FFTPIM_K1=gather|taps|ell overrides
     {
         const char* e = getenv("FFTPIM_K1");
-        if (!e || std::string(e) == "ell") {
+        if (!P->k1_lines && (!e || std::string(e) == "ell")) {
             EvalArgs a = eval_args(P, nullptr, nullptr, FFTPIM_NEAR);
             const int64_t rows = (int64_t)a.knx * dims[1] * dims[2];
             const int64_t nsl = (rows + 31) / 32;
@@ -1234,6 +1264,9 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.k1_q = k1_caller_order(P) ? a.q : P->q_sorted;
     a.k1_idx = P->k1_orig && !k1_caller_order(P) ? P->k1_idx_sorted : P->k1_idx;
     a.k1_wgt = P->k1_wgt;
+    a.k1_pos = P->k1_lines && !P->src_rec ? P->src_pos_s : nullptr;
+    a.k1_rec = P->src_rec;
+    a.obs_pos = P->obs_pos_pass ? P->obs_pos_s : nullptr;
     a.kx0 = 0;
     a.knx = P->near_g.n[0];
     a.gx0 = 0;
@@ -1249,6 +1282,7 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
         a.obs_start = P->obs_start + 3 * i0;
         a.obs_fw = P->obs_fw + i0 * 3 * WF;
         a.obs_fstart = P->obs_fstart + 3 * i0;
+        if (a.obs_pos) a.obs_pos = P->obs_pos_s + 3 * i0;
         a.src_fw = P->src_fw + i0 * 3 * WF;
         a.src_fstart = P->src_fstart + 3 * i0;
         a.far_q = P->q_sorted + i0;

@@ -124,6 +124,9 @@ struct EvalArgs {
     const int* k1_idx;          // source index per entry (into k1_q)
     const double* k1_wgt;       // weight product per entry
     const cplx* k1_q;           // charges K1 reads: q_sorted, or q itself (k1_orig)
+    const double* k1_pos;       // K1 line sweep, staged (non-null selects it): sorted positions
+    const double* k1_rec;       // K1 line sweep, independent threads (non-null selects it): stencil records
+    const double* obs_pos;      // observer pass with in-kernel stencils (non-null selects it)
     const cplx* interp_grid;    // near potentials on the grid, indexed (((x-gx0)*gi1 + y)*gi2 + z)
     int gi1, gi2;
     int gx0;
@@ -165,6 +168,13 @@ void launch_k1_count(const EvalArgs& a, int* cnt_row, int* cnt_sorted, int* row_
 void launch_k1_fill(const EvalArgs& a, const int* row_of, const int64_t* off, const int* remap, int* idx,
                     double* wgt, cudaStream_t s);
 void launch_spectrum_mul(const EvalArgs& a, cudaStream_t s);
+// ---- line-sweep K1 and sorted positions (line_kernels.cu)
+bool launch_k1_lines(const EvalArgs& a, const double* pos, cudaStream_t s);
+bool launch_k1_lines_g(const EvalArgs& a, const double* rec, cudaStream_t s);
+int stencil_record_width(int W);
+void launch_stencil_records(const double* w, const int* start, int64_t n, int W, double* rec, cudaStream_t s);
+void launch_gather_pos(const double* pos, const int* perm, int64_t n, double* out, cudaStream_t s);
+bool launch_observers_pos(const EvalArgs& a, const double* pos, cudaStream_t s, int mode);
 void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);

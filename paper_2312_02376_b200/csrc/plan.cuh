@@ -125,6 +125,11 @@ struct FftpimPlan {
     int* src_start = nullptr;     // (N, 3) near stencil starts, sorted order
     double* obs_w = nullptr;      // observers (aliases src_* if same_points)
     int* obs_start = nullptr;
+    double* src_pos_s = nullptr;  // (N, 3) positions in sorted order (K1 line sweep computes stencils)
+    bool k1_lines = false;        // K1 = line sweep (line_kernels.cu)
+    double* src_rec = nullptr;    // (N, (3W+2)&~1) stencil records for the thread-independent line sweep
+    double* obs_pos_s = nullptr;  // (M, 3) observer positions, sorted (aliases src_pos_s if same points)
+    bool obs_pos_pass = false;    // observer pass computes its stencils from obs_pos_s
     double* src_fw = nullptr;     // (N, 3, Wf) far source-grid weights
     int* src_fstart = nullptr;
     double* obs_fw = nullptr;     // far observer-grid weights

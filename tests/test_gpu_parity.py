@@ -69,6 +69,33 @@ def test_small_case_parity(fp, name):
     assert rel_l2(fp.eval_far(plan.far, q), g["u_far"]) <= TOL
 
 
+@pytest.mark.parametrize("k1", ["lines", "lines_smem"])
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_small_case_parity_point_paths(fp, name, k1, monkeypatch):
+    """The large-N evaluation paths forced on every small case: K1 as a line
+    sweep (line_kernels.cu: plan stencil records, or stencils computed from the
+    sorted positions) and the observer pass computing its stencils from the
+    sorted positions.  Same potentials as the reference (1e-10) and as the
+    default small-N paths (ELL K1, stored-weight observer pass) to 1e-13."""
+    case = SMALL_CASES[name]
+    g = golden(f"small_{name}.npz")
+    pos, q, obs = case_inputs(name)
+    cfg, box, src, ob, prm = ref_objects(fp, case, pos, q, obs)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        base = fp.build_plan(cfg, box, src, ob, prm)
+        monkeypatch.setenv("FFTPIM_K1", k1)
+        monkeypatch.setenv("FFTPIM_OBS", "pos")
+        plan = fp.build_plan(cfg, box, src, ob, prm)
+    u = plan.evaluate(q)
+    assert rel_l2(u, g["u"]) <= TOL
+    assert rel_l2(u, base.evaluate(q)) <= 1e-13
+    assert rel_l2(fp.eval_near(plan.near, q), g["u_near"]) <= TOL
+    assert rel_l2(fp.eval_far(plan.far, q), g["u_far"]) <= TOL
+    np.testing.assert_array_equal(plan.evaluate(q), u)   # bitwise reproducible
+
+
 def _full(fp, c):
     from paper_2312_02376_b200.workloads import CONFIGS, make_inputs
     w = CONFIGS[c]

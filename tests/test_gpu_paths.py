@@ -2,8 +2,9 @@
 same plan geometry):
 
 * K1: the plan-time sliced-ELL operator vs the computed (gather / tiled /
-  tap-major) projections -- the ELL rows keep the gather order and weight
-  expression, so the potentials agree to rounding of the exact-zero padding;
+  tap-major / line-sweep) projections -- the ELL rows keep the gather order and
+  weight expression, so the potentials agree to rounding of the exact-zero
+  padding; the line sweep sums in another fixed order (1e-13);
 * K2: the register-resident column FFTs vs the shared-memory Stockham stages
   vs cuFFT;
 * the host entry with pinned buffers (one graph: upload, evaluation,
@@ -44,6 +45,11 @@ def test_k1_ell_matches_computed_projection(case, tmp_path):
     u_gat, i_gat = run_variant(case, {"FFTPIM_K1": "gather"}, tmp_path, "gather")
     assert i_ell["k1_ell"] and not i_gat["k1_ell"]
     assert rel_l2(u_ell, u_gat) <= 1e-14
+    # line sweep with in-kernel stencils (line_kernels.cu): same weights, another
+    # fixed summation order
+    u_lin, i_lin = run_variant(case, {"FFTPIM_K1": "lines"}, tmp_path, "lines")
+    assert not i_lin["k1_ell"]
+    assert rel_l2(u_lin, u_gat) <= 1e-13
     if case in ("c1", "blobs3d"):
         u_tap, i_tap = run_variant(case, {"FFTPIM_K1": "taps"}, tmp_path, "taps")
         assert rel_l2(u_ell, u_tap) <= 1e-13
