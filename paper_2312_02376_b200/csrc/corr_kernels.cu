@@ -472,6 +472,8 @@ static void launch_observers_lpo(const EvalArgs& a, cudaStream_t s, int mode) {
 // order >= 4, 2 otherwise (measured: C2 / C5 observer pass 10-30 % faster)
 void launch_observers(const EvalArgs& a, cudaStream_t s, int mode) {
     if (a.M == 0) return;
+    if (a.obs_pos && a.obs_cell_start && launch_observers_tile(a, a.obs_pos, a.obs_cell_start, a.obs_i0, s, mode))
+        return;
     if (a.obs_pos && launch_observers_pos(a, a.obs_pos, s, mode)) return;
     // 5-tap (order 4) stencils: 13 entries per lane at 2 lanes spill under the
     // 64-register budget, so those keep 4 lanes

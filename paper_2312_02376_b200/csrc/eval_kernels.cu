@@ -690,21 +690,39 @@ __global__ void __launch_bounds__(256) k_far_project(EvalArgs a) {
         __syncwarp();
     };
     const int64_t stride = (int64_t)gridDim.x * warps * 32;
-    for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < a.far_n; base += stride) {
-        const int64_t p = base + lane;
-        __syncwarp();
+    // the next batch's weights, charge and starts are loaded into registers while
+    // this batch is accumulated (one global round trip per batch, overlapped)
+    double nw[3 * WF], nq[2];
+    int ns[3];
+    auto fetch = [&](int64_t p) {
         if (p < a.far_n) {
             const double* w = a.src_fw + p * 3 * WF;
 #pragma unroll
-            for (int j = 0; j < 3 * WF; ++j) stage[lane * REC + j] = w[j];
-            const cplx qv = a.far_q[p];
-            stage[lane * REC + 3 * WF] = qv.re;
-            stage[lane * REC + 3 * WF + 1] = qv.im;
-            sstart[lane * 3] = a.src_fstart[3 * p];
-            sstart[lane * 3 + 1] = a.src_fstart[3 * p + 1];
-            sstart[lane * 3 + 2] = a.src_fstart[3 * p + 2];
+            for (int j = 0; j < 3 * WF; ++j) nw[j] = __ldg(w + j);
+            const double2 qv = __ldg(reinterpret_cast<const double2*>(a.far_q + p));
+            nq[0] = qv.x;
+            nq[1] = qv.y;
+            ns[0] = __ldg(a.src_fstart + 3 * p);
+            ns[1] = __ldg(a.src_fstart + 3 * p + 1);
+            ns[2] = __ldg(a.src_fstart + 3 * p + 2);
+        }
+    };
+    int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32;
+    fetch(base + lane);
+    for (; base < a.far_n; base += stride) {
+        const int64_t p = base + lane;
+        __syncwarp();
+        if (p < a.far_n) {
+#pragma unroll
+            for (int j = 0; j < 3 * WF; ++j) stage[lane * REC + j] = nw[j];
+            stage[lane * REC + 3 * WF] = nq[0];
+            stage[lane * REC + 3 * WF + 1] = nq[1];
+            sstart[lane * 3] = ns[0];
+            sstart[lane * 3 + 1] = ns[1];
+            sstart[lane * 3 + 2] = ns[2];
         }
         __syncwarp();
+        fetch(base + stride + lane);
         const int cnt = (int)min((int64_t)32, a.far_n - base);
         for (int j = 0; j < cnt; ++j) {
             const double* r = stage + j * REC;
@@ -761,6 +779,7 @@ static void far_project_launch(const EvalArgs& a, size_t smem, cudaStream_t s) {
 }
 
 void launch_far_project(const EvalArgs& a, cudaStream_t s) {
+    if (a.far_pos && launch_far_project_win(a, a.far_pos, a.far_slots, a.far_win, s)) return;
     const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
     const size_t smem = far_project_smem(nf, a.far_warps, a.fs.order);
     switch (a.fs.order + 1) {

@@ -17,6 +17,8 @@
 // evaluation instead of ~130 n^3 for full transforms.
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "geom.cuh"
 #include "kernels.h"
 
@@ -660,6 +662,127 @@ static bool reg3_launch(const FftStage& st, cudaStream_t s) {
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// L = 512 as 8 x 8 x 8 (E = 8 values per thread, 64 threads per column): three
+// register radix-8 levels with two shared-memory exchanges per direction.
+// n = t + 64 j (t = t1 + 8 t2), k = ka + 8 m1 + 64 m2:
+//   A: thread t:          DFT_8 over j  -> ka,  x w_512^(t ka)
+//   B: thread (ka, t1):   DFT_8 over t2 -> m1,  x w_64^(t1 m1)
+//   C: thread (ka, m1):   DFT_8 over t1 -> m2
+// The fused x stage multiplies by the spectrum in layout C and runs the three
+// levels backwards (conjugate twiddles) to the loading layout.  8 complex values
+// per thread instead of 32: ~64 registers, six times the resident warps of the
+// E = 32 kernel, at twice its shared-memory exchanges.
+#define R8_NT 256
+template <bool ZC>
+__global__ void __launch_bounds__(R8_NT) k_fft_r8x3(FftStage st) {
+    constexpr int CPB = R8_NT / 64, AS = 65, BS = 9;   // row strides of the two exchange layouts
+    extern __shared__ cplx xs8[];
+    const int c = ZC ? threadIdx.x / 64 : threadIdx.x % CPB;
+    const int t = ZC ? threadIdx.x % 64 : threadIdx.x / CPB;
+    const int col = blockIdx.x * CPB + c;
+    const bool okc = col < st.nb0;
+    cplx* buf = xs8 + c * (8 * AS > 64 * BS ? 8 * AS : 64 * BS);
+    const cplx* __restrict__ in = st.in + (int64_t)blockIdx.y * st.in_s1 + (int64_t)col * st.in_s0;
+    cplx* out = st.out + (int64_t)blockIdx.y * st.out_s1 + (int64_t)col * st.out_s0;
+    const int hi = t >> 3, lo = t & 7;   // level B/C thread coordinates (ka, t1) / (ka, m1)
+    cplx a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int i = t + 64 * j;
+        a[j] = (okc && i < st.lin) ? in[(int64_t)i * st.in_stride] : mk(0.0);
+    }
+    auto forward = [&](auto sgn) {
+        constexpr int SG = decltype(sgn)::value;
+        dft_reg<8, SG>(a);                                   // A
+#pragma unroll
+        for (int ka = 1; ka < 8; ++ka) a[ka] = a[ka] * twl<SG>(st.tw, t * ka);
+#pragma unroll
+        for (int ka = 0; ka < 8; ++ka) buf[ka * AS + t] = a[ka];
+        __syncthreads();
+#pragma unroll
+        for (int t2 = 0; t2 < 8; ++t2) a[t2] = buf[hi * AS + lo + 8 * t2];
+        dft_reg<8, SG>(a);                                   // B (ka = hi, t1 = lo)
+#pragma unroll
+        for (int m1 = 1; m1 < 8; ++m1) a[m1] = a[m1] * twl<SG>(st.tw, 8 * lo * m1);
+        __syncthreads();
+#pragma unroll
+        for (int m1 = 0; m1 < 8; ++m1) buf[(hi * 8 + m1) * BS + lo] = a[m1];
+        __syncthreads();
+#pragma unroll
+        for (int t1 = 0; t1 < 8; ++t1) a[t1] = buf[(hi * 8 + lo) * BS + t1];
+        dft_reg<8, SG>(a);                                   // C (ka = hi, m1 = lo) -> m2
+    };
+    // layout C: value m2 of thread (ka = hi, m1 = lo) is X[hi + 8 lo + 64 m2]
+    if (st.spec) {
+        forward(std::integral_constant<int, -1>());
+        int64_t fcol = col;
+        if (st.fold_y | st.fold_z) {
+            int ky = col / st.spec_L2, kz = col - ky * st.spec_L2;
+            if (st.fold_y && 2 * ky > st.fold_y) ky = st.fold_y - ky;
+            if (st.fold_z && 2 * kz > st.fold_z) kz = st.fold_z - kz;
+            fcol = (int64_t)ky * st.spec_L2 + kz;
+        }
+        const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + fcol * st.spec_s0;
+        if (okc) {
+#pragma unroll
+            for (int m2 = 0; m2 < 8; ++m2) a[m2] = a[m2] * sp[(int64_t)(hi + 8 * lo + 64 * m2) * st.spec_stride];
+        }
+        dft_reg<8, +1>(a);                                   // C^-1: m2 -> t1
+        __syncthreads();
+#pragma unroll
+        for (int t1 = 0; t1 < 8; ++t1) buf[(hi * 8 + lo) * BS + t1] = a[t1];
+        __syncthreads();
+#pragma unroll
+        for (int m1 = 0; m1 < 8; ++m1) a[m1] = buf[(hi * 8 + m1) * BS + lo];   // thread (ka, t1)
+#pragma unroll
+        for (int m1 = 1; m1 < 8; ++m1) a[m1] = a[m1] * twl<+1>(st.tw, 8 * lo * m1);
+        dft_reg<8, +1>(a);                                   // B^-1: m1 -> t2
+        __syncthreads();
+#pragma unroll
+        for (int t2 = 0; t2 < 8; ++t2) buf[hi * AS + lo + 8 * t2] = a[t2];
+        __syncthreads();
+#pragma unroll
+        for (int ka = 0; ka < 8; ++ka) a[ka] = buf[ka * AS + t];   // thread t
+#pragma unroll
+        for (int ka = 1; ka < 8; ++ka) a[ka] = a[ka] * twl<+1>(st.tw, t * ka);
+        dft_reg<8, +1>(a);                                   // A^-1: ka -> j
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = t + 64 * j;
+            if (okc && i < st.lout) out[(int64_t)i * st.out_stride] = a[j];
+        }
+        return;
+    }
+    if (st.sign < 0)
+        forward(std::integral_constant<int, -1>());
+    else
+        forward(std::integral_constant<int, +1>());
+#pragma unroll
+    for (int m2 = 0; m2 < 8; ++m2) {
+        const int k = hi + 8 * lo + 64 * m2;
+        if (okc && k < st.lout) out[(int64_t)k * st.out_stride] = a[m2];
+    }
+}
+
+static bool r8x3_launch(const FftStage& st, cudaStream_t s) {
+    if (st.L != 512) return false;
+    constexpr int CPB = R8_NT / 64;
+    const size_t smem = (size_t)CPB * (8 * 65 > 64 * 9 ? 8 * 65 : 64 * 9) * sizeof(cplx);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_fft_r8x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_r8x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid((st.nb0 + CPB - 1) / CPB, st.nb1);
+    if (st.in_stride == 1)
+        k_fft_r8x3<true><<<grid, R8_NT, smem, s>>>(st);
+    else
+        k_fft_r8x3<false><<<grid, R8_NT, smem, s>>>(st);
+    return true;
+}
+
 static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
     static const bool off = [] {
         const char* e = getenv("FFTPIM_FFT_REG");
@@ -674,8 +797,12 @@ static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
         const char* e = getenv("FFTPIM_FFT_REG3");
         return !(e && e[0] == '0');
     }();
+    static const bool r8 = [] {   // L = 512 as 8 x 8 x 8 (FFTPIM_FFT_R8=0: the E = 32 two-level kernel)
+        const char* e = getenv("FFTPIM_FFT_R8");
+        return !(e && e[0] == '0');
+    }();
     return reg_launch<64>(st, s) || reg_launch<128>(st, s) || reg_launch<256>(st, s) ||
-           (r512 && reg_launch<512>(st, s)) ||
+           (r512 && r8 && r8x3_launch(st, s)) || (r512 && reg_launch<512>(st, s)) ||
            (r3 && (reg3_launch<32>(st, s) || reg3_launch<64>(st, s) || reg3_launch<128>(st, s) ||
                    reg3_launch<256>(st, s)));
 }

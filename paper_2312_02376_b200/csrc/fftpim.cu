@@ -671,7 +671,19 @@ void build(FftpimPlan* P) {
         // observer pass with stencils from sorted positions (line_kernels.cu) for
         // large observer sets; FFTPIM_OBS=pos|weights overrides
         const char* e = getenv("FFTPIM_OBS");
-        P->obs_pos_pass = W >= 3 && W <= 6 && WF >= 3 && WF <= 5 && (e ? std::string(e) == "pos" : false);
+        const std::string om = e ? e : "weights";
+        P->obs_pos_pass = W >= 3 && W <= 6 && WF >= 3 && WF <= 5 && (om == "pos" || om == "tile");
+        P->obs_tile = P->obs_pos_pass && om == "tile";
+        if (P->obs_tile) {
+            if (same) {
+                P->obs_cell_start = P->cell_start;
+            } else {
+                P->obs_cell_start = dalloc<int>(P, prod3(P->near_g.nc) + 1);
+                int* tmp_perm = dalloc<int>(P, M);
+                sort_points(P, d_obs, M, tmp_perm, P->obs_cell_start, s);   // same key, same stable order
+                dfree(P, tmp_perm);
+            }
+        }
         if (P->obs_pos_pass) {
             if (same && P->src_pos_s) {
                 P->obs_pos_s = P->src_pos_s;
@@ -1171,6 +1183,21 @@ void build(FftpimPlan* P) {
         P->far_blocks = blocks;
         P->far_blocks_seq = blocks_seq;
         P->far_partial = dalloc<cplx>(P, (int64_t)blocks_seq * nf);
+        {
+            // windowed far projection from the sorted positions (FFTPIM_FAR=win|warps)
+            const char* e = getenv("FFTPIM_FAR");
+            const bool win = (e ? std::string(e) == "win" : false) && pr.far_order + 1 >= 3 && pr.far_order + 1 <= 5;
+            if (win) {
+                if (!P->src_pos_s) {
+                    P->src_pos_s = dalloc<double>(P, 3 * N);
+                    launch_gather_pos(d_src, P->src_perm, N, P->src_pos_s, s);
+                }
+                const int64_t nfp = P->sharded ? Mown : N;   // points the far projection takes
+                const int64_t nch = (nfp + far_win_chunk(nfp) - 1) / far_win_chunk(nfp);
+                P->far_slots = dalloc<cplx>(P, std::max<int64_t>(nch, 1) * nf);
+                P->far_win = dalloc<int>(P, std::max<int64_t>(nch, 1) * 6);
+            }
+        }
         P->far_qg = dalloc<cplx>(P, nf);
         P->far_ug = dalloc<cplx>(P, nf);
     }
@@ -1257,6 +1284,9 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.far_warps = P->far_warps;
     a.far_q = P->q_sorted;
     a.far_n = P->N;
+    a.far_pos = P->far_slots ? P->src_pos_s : nullptr;
+    a.far_slots = P->far_slots;
+    a.far_win = P->far_win;
     a.k1_scratch = P->k1_scratch;
     a.k1_cnt = P->k1_cnt;
     a.k1_row = P->k1_row;
@@ -1267,6 +1297,8 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.k1_pos = P->k1_lines && !P->src_rec ? P->src_pos_s : nullptr;
     a.k1_rec = P->src_rec;
     a.obs_pos = P->obs_pos_pass ? P->obs_pos_s : nullptr;
+    a.obs_cell_start = P->obs_tile ? P->obs_cell_start : nullptr;
+    a.obs_i0 = 0;
     a.kx0 = 0;
     a.knx = P->near_g.n[0];
     a.gx0 = 0;
@@ -1283,10 +1315,12 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
         a.obs_fw = P->obs_fw + i0 * 3 * WF;
         a.obs_fstart = P->obs_fstart + 3 * i0;
         if (a.obs_pos) a.obs_pos = P->obs_pos_s + 3 * i0;
+        a.obs_i0 = i0;
         a.src_fw = P->src_fw + i0 * 3 * WF;
         a.src_fstart = P->src_fstart + 3 * i0;
         a.far_q = P->q_sorted + i0;
         a.far_n = P->i1 - P->i0;
+        if (a.far_pos) a.far_pos = P->src_pos_s + 3 * i0;
         a.kx0 = P->X0;
         a.knx = P->n0_loc;
         a.gx0 = P->X0;

@@ -127,6 +127,8 @@ struct EvalArgs {
     const double* k1_pos;       // K1 line sweep, staged (non-null selects it): sorted positions
     const double* k1_rec;       // K1 line sweep, independent threads (non-null selects it): stencil records
     const double* obs_pos;      // observer pass with in-kernel stencils (non-null selects it)
+    const int* obs_cell_start;  // observer cell CSR (global sorted indices): grid-tile observer pass
+    int64_t obs_i0;             // first observer of this plan (slab shard) in the global sorted order
     const cplx* interp_grid;    // near potentials on the grid, indexed (((x-gx0)*gi1 + y)*gi2 + z)
     int gi1, gi2;
     int gx0;
@@ -154,6 +156,9 @@ struct EvalArgs {
     cplx* far_ug;
     int far_blocks, far_warps;
     const cplx* far_q;          // sources projected onto the far grid (own range for shards)
+    const double* far_pos;      // their sorted positions (non-null: windowed far projection)
+    cplx* far_slots;            // windowed far projection: per-chunk windows
+    int* far_win;
     int64_t far_n;
     cplx* obs_pre;              // far + K4 fix-up per sorted observer (split observer pass)
     const cplx* sw_corr;        // sweep: K4 sums (M, E) replace the segment fix-up
@@ -175,6 +180,10 @@ int stencil_record_width(int W);
 void launch_stencil_records(const double* w, const int* start, int64_t n, int W, double* rec, cudaStream_t s);
 void launch_gather_pos(const double* pos, const int* perm, int64_t n, double* out, cudaStream_t s);
 bool launch_observers_pos(const EvalArgs& a, const double* pos, cudaStream_t s, int mode);
+bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, int* win, cudaStream_t s);
+int far_win_chunk(int64_t n);
+bool launch_observers_tile(const EvalArgs& a, const double* pos, const int* ocs, int64_t i0, cudaStream_t s,
+                           int mode);
 void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);

@@ -91,103 +91,158 @@ struct K1Lines {
 template <int W>
 size_t k1_lines_smem(int cap) {
     using T = K1Lines<W>;
-    return (size_t)cap * T::REC * sizeof(double) + (size_t)(T::ROWS * (T::CELLS + 1) + T::ROWS + 1) * sizeof(int);
+    return (size_t)cap * T::REC * sizeof(double) + (size_t)(2 * T::ROWS * (T::CELLS + 1) + T::ROWS + 1) * sizeof(int);
 }
 
+#define K1L_PF 3   // staged points per thread per piece held in flight (cap <= K1L_PF * K1L_NT)
 template <int W>
-__global__ void __launch_bounds__(K1L_NT, 2) k_k1_lines(EvalArgs a, const double* __restrict__ pos, int xc,
-                                                        int cap, double rh0, double rh1, double rh2) {
+__global__ void __launch_bounds__(K1L_NT, 3) k_k1_lines(EvalArgs a, const double* __restrict__ pos, int xc,
+                                                        int n_items, int cap, double rh0, double rh1, double rh2) {
     using T = K1Lines<W>;
-    constexpr int ROWS = T::ROWS, CELLS = T::CELLS, REC = T::REC, R = K1L_R;
+    constexpr int ROWS = T::ROWS, CELLS = T::CELLS, REC = T::REC, R = K1L_R, LCS = ROWS * (CELLS + 1);
+    constexpr int LPT = (LCS + K1L_NT - 1) / K1L_NT;   // cell starts per thread
     extern __shared__ double k1l_smem[];
     double* rec = k1l_smem;                                       // cap x REC
-    int* lcs = reinterpret_cast<int*>(rec + (size_t)cap * REC);  // ROWS x (CELLS + 1) global point starts
-    int* soff = lcs + ROWS * (CELLS + 1);                         // ROWS + 1 staged row offsets
+    int* lcs2 = reinterpret_cast<int*>(rec + (size_t)cap * REC);  // 2 x ROWS x (CELLS + 1) global point starts
+    int* soff = lcs2 + 2 * LCS;                                   // ROWS + 1 staged row offsets
     const StencilGeom& g = a.g;
     const LagrangeDen<W> L;
     const int tid = threadIdx.x;
     const int ly = tid / (K1L_TZ / R), lzg = tid % (K1L_TZ / R);
-    const int y0 = blockIdx.y * K1L_TY, z0 = blockIdx.x * K1L_TZ;
-    const int y = y0 + ly, zb = z0 + lzg * R;
-    const int xo0 = a.kx0 + blockIdx.z * xc;
-    const int xo1 = min(xo0 + xc, a.kx0 + a.knx);
-    const int wx0 = g.w[0];
-    const int sx_lo = max(xo0 - (wx0 - 1), 0);
-    const int sx_hi = min(xo1 - 1, g.nc[0] - 1);
+    const int gz = (g.n[2] + K1L_TZ - 1) / K1L_TZ, gy = (g.n[1] + K1L_TY - 1) / K1L_TY;
     const int nc1 = g.nc[1], nc2 = g.nc[2];
-
-    double wr[R][W], wi[R][W];
+    // cell starts of plane sx for this thread's entries of the reach
+    auto load_lcs = [&](int sx, int y0, int z0, int (&v)[LPT]) {
 #pragma unroll
-    for (int j = 0; j < R; ++j)
+        for (int u = 0; u < LPT; ++u) {
+            const int e = tid + u * K1L_NT;
+            v[u] = 0;
+            if (e < LCS && sx >= 0 && sx < g.nc[0]) {
+                const int r = e / (CELLS + 1), c = e - r * (CELLS + 1);
+                const int sy = y0 - (W - 1) + r;
+                if (sy >= 0 && sy < nc1) {
+                    const int sz = min(max(z0 - (W - 1) + c, 0), nc2);
+                    v[u] = __ldg(a.cell_start + ((int64_t)sx * nc1 + sy) * nc2 + sz);
+                }
+            }
+        }
+    };
+    auto put_lcs = [&](int* dst, const int (&v)[LPT]) {
 #pragma unroll
-        for (int ia = 0; ia < W; ++ia) wr[j][ia] = wi[j][ia] = 0.0;
-
-    auto store = [&](int x, int slot) {
-        if (x < xo0 || x >= xo1 || y >= g.n[1]) return;
-        cplx* dst = a.k1_out + ((int64_t)(x - a.kx0) * a.go1 + y) * a.go2;
+        for (int u = 0; u < LPT; ++u) {
+            const int e = tid + u * K1L_NT;
+            if (e < LCS) dst[e] = v[u];
+        }
+    };
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int tz = item % gz, ty = (item / gz) % gy, tx = item / (gz * gy);
+        const int y0 = ty * K1L_TY, z0 = tz * K1L_TZ;
+        const int y = y0 + ly, zb = z0 + lzg * R;
+        const int xo0 = a.kx0 + tx * xc;
+        const int xo1 = min(xo0 + xc, a.kx0 + a.knx);
+        const int sx_lo = max(xo0 - (g.w[0] - 1), 0);
+        const int sx_hi = min(xo1 - 1, g.nc[0] - 1);
+        double wr[R][W], wi[R][W];
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            if (zb + j < g.n[2]) {
 #pragma unroll
-                for (int ia = 0; ia < W; ++ia)
-                    if (ia == slot) dst[zb + j] = cplx{wr[j][ia], wi[j][ia]};
-            }
-    };
-
-    for (int sx = sx_lo; sx <= sx_hi; ++sx) {
-        // global point range of every reach cell: row r = sy - (y0 - W + 1),
-        // cell c = sz - (z0 - W + 1); cells past the axis clamp to the row end
-        for (int e = tid; e < ROWS * (CELLS + 1); e += K1L_NT) {
-            const int r = e / (CELLS + 1), c = e - r * (CELLS + 1);
-            const int sy = y0 - (W - 1) + r;
-            int v = 0;
-            if (sy >= 0 && sy < nc1) {
-                const int sz = min(max(z0 - (W - 1) + c, 0), nc2);
-                v = a.cell_start[((int64_t)sx * nc1 + sy) * nc2 + sz];
-            }
-            lcs[e] = v;
-        }
-        __syncthreads();
-        if (tid < 32) {
-            int len = tid < ROWS ? lcs[tid * (CELLS + 1) + CELLS] - lcs[tid * (CELLS + 1)] : 0;
-            int inc = len;
+            for (int ia = 0; ia < W; ++ia) wr[j][ia] = wi[j][ia] = 0.0;
+        auto store = [&](int x, int slot) {
+            if (x < xo0 || x >= xo1 || y >= g.n[1]) return;
+            cplx* dst = a.k1_out + ((int64_t)(x - a.kx0) * a.go1 + y) * a.go2;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, inc, o);
-                if (tid >= o) inc += v;
-            }
-            if (tid < ROWS) soff[tid + 1] = inc;
-            if (tid == 0) soff[0] = 0;
+            for (int j = 0; j < R; ++j)
+                if (zb + j < g.n[2]) {
+#pragma unroll
+                    for (int ia = 0; ia < W; ++ia)
+                        if (ia == slot) dst[zb + j] = cplx{wr[j][ia], wi[j][ia]};
+                }
+        };
+        {
+            int v[LPT];
+            load_lcs(sx_lo, y0, z0, v);
+            __syncthreads();   // previous item's last readers of lcs2 / soff / rec
+            put_lcs(lcs2 + (sx_lo & 1) * LCS, v);
         }
-        __syncthreads();
-        const int total = soff[ROWS];
-        for (int p0 = 0; p0 < total; p0 += cap) {
-            const int pc = min(cap, total - p0);
-            for (int e = tid; e < pc; e += K1L_NT) {
-                const int idx = p0 + e;
-                int r = 0;
-#pragma unroll 1
-                while (r + 1 < ROWS && soff[r + 1] <= idx) ++r;
-                const int64_t gi = lcs[r * (CELLS + 1)] + (idx - soff[r]);
-                double* rp = rec + (size_t)e * REC;
-                const cplx qv = a.q_sorted[gi];
-                rp[0] = qv.re;
-                rp[1] = qv.im;
-                fast_stencil<W>(pos[3 * gi], g.n[0], g.origin[0], g.h[0], rh0, L, rp + 2);
-                fast_stencil<W>(pos[3 * gi + 1], g.n[1], g.origin[1], g.h[1], rh1, L, rp + 2 + W);
-                const int sz = fast_stencil<W>(pos[3 * gi + 2], g.n[2], g.origin[2], g.h[2], rh2, L, rp + 2 + 2 * W);
-                rp[2 + 3 * W] = (double)sz;
+        for (int sx = sx_lo; sx <= sx_hi; ++sx) {
+            const int* lcs = lcs2 + (sx & 1) * LCS;
+            __syncthreads();
+            if (tid < 32) {   // staged row offsets (ROWS <= 32)
+                const int len = tid < ROWS ? lcs[tid * (CELLS + 1) + CELLS] - lcs[tid * (CELLS + 1)] : 0;
+                int inc = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (tid >= o) inc += t;
+                }
+                if (tid < ROWS) soff[tid + 1] = inc;
+                if (tid == 0) soff[0] = 0;
             }
             __syncthreads();
+            const int total = soff[ROWS];
+            // the next plane's cell starts are in flight during this plane
+            int nxt[LPT];
+            load_lcs(sx + 1, y0, z0, nxt);
+            for (int p0 = 0; p0 < total; p0 += cap) {
+                const int pc = min(cap, total - p0);
+                // all loads of this thread's staged points first, then the stencils
+                int64_t gi[K1L_PF];
+                double px[K1L_PF], py[K1L_PF], pz[K1L_PF];
+                double2 qq[K1L_PF];
+#pragma unroll
+                for (int u = 0; u < K1L_PF; ++u) {
+                    const int e = tid + u * K1L_NT;
+                    gi[u] = -1;
+                    if (e < pc) {
+                        const int idx = p0 + e;
+                        int lo = 0, hi = ROWS;   // soff[lo] <= idx < soff[lo + 1]
+#pragma unroll
+                        for (int st = 0; st < 5; ++st) {
+                            const int mid = (lo + hi) >> 1;
+                            if (hi - lo > 1) {
+                                if (soff[mid] <= idx) lo = mid; else hi = mid;
+                            }
+                        }
+                        gi[u] = lcs[lo * (CELLS + 1)] + (idx - soff[lo]);
+                        px[u] = __ldg(pos + 3 * gi[u]);
+                        py[u] = __ldg(pos + 3 * gi[u] + 1);
+                        pz[u] = __ldg(pos + 3 * gi[u] + 2);
+                        qq[u] = __ldg(reinterpret_cast<const double2*>(a.q_sorted + gi[u]));
+                    }
+                }
+                if (p0) __syncthreads();   // the previous piece's readers of rec
+#pragma unroll
+                for (int u = 0; u < K1L_PF; ++u) {
+                    if (gi[u] < 0) continue;
+                    double* rp = rec + (size_t)(tid + u * K1L_NT) * REC;
+                    rp[0] = qq[u].x;
+                    rp[1] = qq[u].y;
+                    fast_stencil<W>(px[u], g.n[0], g.origin[0], g.h[0], rh0, L, rp + 2);
+                    fast_stencil<W>(py[u], g.n[1], g.origin[1], g.h[1], rh1, L, rp + 2 + W);
+                    rp[2 + 3 * W] = (double)fast_stencil<W>(pz[u], g.n[2], g.origin[2], g.h[2], rh2, L, rp + 2 + 2 * W);
+                }
+                __syncthreads();
+                // this thread's point ranges of the W rows it reads, flattened
+                // into one loop (less lane divergence than W separate loops)
+                int b0[W], pre[W + 1];
+                pre[0] = 0;
+#pragma unroll
+                for (int ib = 0; ib < W; ++ib) {
+                    const int r = ly + (W - 1) - ib;
+                    const int* row = lcs + r * (CELLS + 1);
+                    const int base = soff[r] - row[0] - p0;
+                    b0[ib] = max(base + row[lzg * R], 0);
+                    pre[ib + 1] = pre[ib] + max(min(base + row[lzg * R + R + W - 1], pc) - b0[ib], 0);
+                }
 #pragma unroll 1
-            for (int ib = 0; ib < W; ++ib) {
-                const int r = ly + (W - 1) - ib;
-                const int* row = lcs + r * (CELLS + 1);
-                const int base = soff[r] - row[0] - p0;
-                const int b0 = max(base + row[lzg * R], 0);
-                const int b1 = min(base + row[lzg * R + R + W - 1], pc);
-#pragma unroll 1
-                for (int k = b0; k < b1; ++k) {
+                for (int t = 0; t < pre[W]; ++t) {
+                    int ib = 0;
+#pragma unroll
+                    for (int u = 1; u < W; ++u) ib += t >= pre[u];
+                    int k = b0[0] + t;
+#pragma unroll
+                    for (int u = 1; u < W; ++u)
+                        if (ib == u) k = b0[u] + (t - pre[u]);
                     const double* rp = rec + (size_t)k * REC;
                     const double2 qv = *reinterpret_cast<const double2*>(rp);
                     double wx[W];
@@ -195,12 +250,12 @@ __global__ void __launch_bounds__(K1L_NT, 2) k_k1_lines(EvalArgs a, const double
                     for (int ia = 0; ia < W; ++ia) wx[ia] = rp[2 + ia];
                     const double wy = rp[2 + W + ib];
                     const int sz = (int)rp[2 + 3 * W];
+                    const double qyr = qv.x * wy, qyi = qv.y * wy;
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         const int ic = zb + j - sz;
                         const double wz = (unsigned)ic < (unsigned)W ? rp[2 + 2 * W + ic] : 0.0;
-                        const double t = wy * wz;
-                        const double cr = qv.x * t, ci = qv.y * t;
+                        const double cr = qyr * wz, ci = qyi * wz;
 #pragma unroll
                         for (int ia = 0; ia < W; ++ia) {
                             wr[j][ia] = fma(cr, wx[ia], wr[j][ia]);
@@ -209,46 +264,59 @@ __global__ void __launch_bounds__(K1L_NT, 2) k_k1_lines(EvalArgs a, const double
                     }
                 }
             }
-            __syncthreads();
-        }
-        // node sx has all its planes: store it, shift the windows
-        store(sx, 0);
+            put_lcs(lcs2 + ((sx + 1) & 1) * LCS, nxt);
+            // node sx has all its planes: store it, shift the windows
+            store(sx, 0);
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
+            for (int j = 0; j < R; ++j) {
 #pragma unroll
-            for (int ia = 0; ia + 1 < W; ++ia) {
-                wr[j][ia] = wr[j][ia + 1];
-                wi[j][ia] = wi[j][ia + 1];
+                for (int ia = 0; ia + 1 < W; ++ia) {
+                    wr[j][ia] = wr[j][ia + 1];
+                    wi[j][ia] = wi[j][ia + 1];
+                }
+                wr[j][W - 1] = wi[j][W - 1] = 0.0;
             }
-            wr[j][W - 1] = wi[j][W - 1] = 0.0;
         }
-    }
-    // nodes past the last start plane (x > nc0 - 1) or past the chunk's sweep
+        // nodes past the last start plane (x > nc0 - 1) or past the chunk's sweep
 #pragma unroll
-    for (int ia = 0; ia + 1 < W; ++ia) store(sx_hi + 1 + ia, ia);
+        for (int ia = 0; ia + 1 < W; ++ia) store(sx_hi + 1 + ia, ia);
+    }
 }
 
 template <int W>
 static void k1_lines_launch(const EvalArgs& a, const double* pos, cudaStream_t s) {
-    static int cap = 0;
+    static int cap = 0, per_sm = 0;
     static size_t smem = 0;
     if (!cap) {
-        cap = 448;
-        if (const char* e = getenv("FFTPIM_K1L_CAP")) cap = std::max(64, atoi(e));
+        cap = K1L_PF * K1L_NT;
+        if (const char* e = getenv("FFTPIM_K1L_CAP")) cap = std::max(64, std::min(cap, atoi(e)));
         smem = k1_lines_smem<W>(cap);
         cudaFuncSetAttribute(k_k1_lines<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_k1_lines<W>, K1L_NT, smem);
+        per_sm = std::max(per_sm, 1);
     }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int slots = sms * per_sm;
     const int gz = (a.g.n[2] + K1L_TZ - 1) / K1L_TZ, gy = (a.g.n[1] + K1L_TY - 1) / K1L_TY;
-    // chunks of >= 2 (W - 1) planes (the warm-up planes are redone per chunk),
-    // enough chunks for ~4 blocks per SM
-    int xc = (int)(((int64_t)a.knx * gy * gz + 591) / 592);
-    xc = std::max(xc, 2 * (W - 1));
+    // chunk length: minimise rounds x planes swept per item (W - 1 warm-up planes each)
+    int xc = std::max(a.knx, 1), best = 1 << 30;
+    for (int c = std::min(2 * (W - 1), a.knx); c <= a.knx; ++c) {
+        const int items = gz * gy * ((a.knx + c - 1) / c);
+        const int rounds = (items + slots - 1) / slots;
+        const int cost = rounds * (c + W - 1);
+        if (cost < best) {
+            best = cost;
+            xc = c;
+        }
+    }
     if (const char* e = getenv("FFTPIM_K1L_XC")) xc = std::max(1, atoi(e));
-    xc = std::min(xc, std::max(a.knx, 1));
-    const int gx = (a.knx + xc - 1) / xc;
+    xc = std::max(1, std::min(xc, std::max(a.knx, 1)));
+    const int items = gz * gy * ((a.knx + xc - 1) / xc);
     const double rh0 = a.g.h[0] > 0 ? 1.0 / a.g.h[0] : 0.0, rh1 = a.g.h[1] > 0 ? 1.0 / a.g.h[1] : 0.0,
                  rh2 = a.g.h[2] > 0 ? 1.0 / a.g.h[2] : 0.0;
-    k_k1_lines<W><<<dim3(gz, gy, gx), K1L_NT, smem, s>>>(a, pos, xc, cap, rh0, rh1, rh2);
+    k_k1_lines<W><<<std::min(items, slots), K1L_NT, smem, s>>>(a, pos, xc, items, cap, rh0, rh1, rh2);
 }
 
 bool launch_k1_lines(const EvalArgs& a, const double* pos, cudaStream_t s) {
@@ -611,4 +679,421 @@ bool launch_observers_pos(const EvalArgs& a, const double* pos, cudaStream_t s, 
         ok = lpo4 ? obsp_near<0, 4>(a, o, s) : obsp_near<0, 2>(a, o, s);
     if (ok) fftpim_count_launch();
     return ok;
+}
+
+// ------------------------------------------------------------- K3 on grid tiles
+// Observer pass for the near interpolation (+ far interpolation and the K4
+// row fix-up, or the precomputed far/fix-up term of the split schedule): a
+// block owns a TX x TY x TZ tile of observer stencil-start cells -- TX * TY rows,
+// each ONE contiguous run of the cell-sorted observers -- and first copies
+// the (TX + W - 1) x (TY + W - 1) x (TZ + W - 1) grid nodes those observers can
+// reach (coalesced z runs) plus the far observer grid into shared memory.
+// Each thread then takes observers, computes their near and far stencils from
+// the sorted position and gathers the 125 (or W^3) taps from the tile:
+// consecutive lanes take consecutive observers of a row, whose taps are
+// consecutive tile words.  The K4 row fix-up is the same fixed-order segment
+// sum as k_observers; every sum has a fixed order.
+#define K3T_TX 4
+#define K3T_TY 4
+#define K3T_TZ 32
+#define K3T_NT 256
+template <int W>
+struct K3Tile {
+    static constexpr int EX = K3T_TX + W - 1, EY = K3T_TY + W - 1, EZ = K3T_TZ + W - 1;
+    static constexpr int NODES = EX * EY * EZ;
+    static constexpr int ROWS = K3T_TX * K3T_TY;
+};
+
+#ifndef K3T_MINB
+#define K3T_MINB 4
+#endif
+template <int W, int WF, int MODE>
+__global__ void __launch_bounds__(K3T_NT, K3T_MINB) k_observers_tile(EvalArgs a, ObsPosArgs o, const int* __restrict__ ocs,
+                                                             int64_t i0, int tsx0, int tnx) {
+    using T = K3Tile<W>;
+    extern __shared__ double k3t_smem[];
+    cplx* tile = reinterpret_cast<cplx*>(k3t_smem);                 // NODES
+    cplx* sfar = tile + T::NODES;                                    // far grid (MODE 0)
+    const bool far = MODE == 0 && (a.parts & FFTPIM_FAR);
+    const int nfx = a.fo.n[0], nfy = a.fo.n[1], nfz = a.fo.n[2];
+    const int nf = far ? nfx * nfy * nfz : 0;
+    int* rbeg = reinterpret_cast<int*>(sfar + nf);                   // ROWS + 1 (row starts, staged order)
+    int* rglo = rbeg + T::ROWS + 1;                                  // ROWS (global first observer)
+    const StencilGeom& g = a.g;
+    const int gz = (g.nc[2] + K3T_TZ - 1) / K3T_TZ, gy = (g.nc[1] + K3T_TY - 1) / K3T_TY;
+    const int bz = blockIdx.x % gz, by = (blockIdx.x / gz) % gy, bx = blockIdx.x / (gz * gy);
+    const int sx0 = tsx0 + bx * K3T_TX, sy0 = by * K3T_TY, sz0 = bz * K3T_TZ;
+    const int nc1 = g.nc[1], nc2 = g.nc[2];
+    const int sxe = min(tsx0 + tnx, g.nc[0]);
+    if (threadIdx.x < 32) {
+        const int r = threadIdx.x;
+        int lo = 0, len = 0;
+        if (r < T::ROWS) {
+            const int sx = sx0 + r / K3T_TY, sy = sy0 + r % K3T_TY;
+            if (sx < sxe && sy < nc1) {
+                const int64_t k = ((int64_t)sx * nc1 + sy) * nc2;
+                lo = ocs[k + sz0];
+                len = ocs[k + min(sz0 + K3T_TZ, nc2)] - lo;
+            }
+        }
+        int inc = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, d);
+            if (r >= d) inc += t;
+        }
+        if (r < T::ROWS) {
+            rbeg[r + 1] = inc;
+            rglo[r] = lo;
+        }
+        if (r == 0) rbeg[0] = 0;
+    }
+    // grid tile: nodes (sx0 + ex, sy0 + ey, sz0 + ez), clipped to the grid
+    {
+        const int m0 = g.n[0], m1 = g.n[1], m2 = g.n[2];
+        for (int e = threadIdx.x; e < T::NODES; e += K3T_NT) {
+            const int ez = e % T::EZ, ey = (e / T::EZ) % T::EY, ex = e / (T::EZ * T::EY);
+            const int x = sx0 + ex, y = sy0 + ey, z = sz0 + ez;
+            cplx v = mk(0.0);
+            if (x < m0 && x < sxe + W - 1 && y < m1 && z < m2)
+                v = a.interp_grid[((int64_t)(x - a.gx0) * a.gi1 + y) * a.gi2 + z];
+            tile[e] = v;
+        }
+        if (far)
+            for (int t = threadIdx.x; t < nf; t += K3T_NT) sfar[t] = a.far_ug[t];
+    }
+    __syncthreads();
+    const int total = rbeg[T::ROWS];
+    const LagrangeDen<W> Ln;
+    const LagrangeDen<WF> Lf;
+    for (int k = threadIdx.x; k < total; k += K3T_NT) {
+        int r = 0;
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {   // ROWS = 16: rbeg[r] <= k < rbeg[r + 1]
+            const int step = 8 >> st;
+            if (rbeg[r + step] <= k) r += step;
+        }
+        const int64_t ig = rglo[r] + (k - rbeg[r]);   // global sorted observer
+        const int64_t i = ig - i0;                    // this plan's (shard's) observer
+        const double px = o.pos[3 * i], py = o.pos[3 * i + 1], pz = o.pos[3 * i + 2];
+        double ar = 0.0, ai = 0.0;
+        if (MODE == 2) {
+            const cplx c = a.obs_pre[i];
+            ar = c.re;
+            ai = c.im;
+        } else if ((a.parts & FFTPIM_NEAR) && a.sw_e >= 0) {
+            const cplx c = a.sw_corr ? a.sw_corr[i * a.sw_E + a.sw_e] : corr_row_sum(a, i);
+            ar = c.re;
+            ai = c.im;
+        }
+        if (a.parts & FFTPIM_NEAR) {
+            // per x plane an independent partial (W accumulator chains in flight),
+            // summed in plane order
+            double wx[W], wy[W], wz[W];
+            const int s0 = fast_stencil<W>(px, g.n[0], g.origin[0], g.h[0], o.rn[0], Ln, wx) - sx0;
+            const int s1 = fast_stencil<W>(py, g.n[1], g.origin[1], g.h[1], o.rn[1], Ln, wy) - sy0;
+            const int s2 = fast_stencil<W>(pz, g.n[2], g.origin[2], g.h[2], o.rn[2], Ln, wz) - sz0;
+            double pr[W], pi[W];
+#pragma unroll
+            for (int ia = 0; ia < W; ++ia) {
+                pr[ia] = pi[ia] = 0.0;
+#pragma unroll
+                for (int ib = 0; ib < W; ++ib) {
+                    const cplx* row = tile + ((s0 + ia) * T::EY + (s1 + ib)) * T::EZ + s2;
+                    const double wxy = wx[ia] * wy[ib];
+#pragma unroll
+                    for (int ic = 0; ic < W; ++ic) {
+                        const cplx v = row[ic];
+                        const double wgt = wxy * wz[ic];
+                        pr[ia] += wgt * v.re;
+                        pi[ia] += wgt * v.im;
+                    }
+                }
+            }
+#pragma unroll
+            for (int ia = 0; ia < W; ++ia) {
+                ar += pr[ia];
+                ai += pi[ia];
+            }
+        }
+        if (far) {
+            double wx[WF], wy[WF], wz[WF];
+            const int s0 = fast_stencil<WF>(px, a.fo.n[0], a.fo.origin[0], a.fo.h[0], o.rf[0], Lf, wx);
+            const int s1 = fast_stencil<WF>(py, a.fo.n[1], a.fo.origin[1], a.fo.h[1], o.rf[1], Lf, wy);
+            const int s2 = fast_stencil<WF>(pz, a.fo.n[2], a.fo.origin[2], a.fo.h[2], o.rf[2], Lf, wz);
+#pragma unroll
+            for (int ia = 0; ia < WF; ++ia) {
+#pragma unroll
+                for (int ib = 0; ib < WF; ++ib) {
+                    const int xx = min(s0 + ia, nfx - 1), yy = min(s1 + ib, nfy - 1);
+                    const cplx* row = sfar + (xx * nfy + yy) * nfz;
+                    const double wxy = wx[ia] * wy[ib];
+#pragma unroll
+                    for (int ic = 0; ic < WF; ++ic) {
+                        const cplx v = row[min(s2 + ic, nfz - 1)];
+                        const double wgt = wxy * wz[ic];
+                        ar += wgt * v.re;
+                        ai += wgt * v.im;
+                    }
+                }
+            }
+        }
+        a.u[a.obs_perm[i]] = cplx{ar, ai};
+    }
+}
+
+template <int W, int WF, int MODE>
+static void obs_tile_launch(const EvalArgs& a, const ObsPosArgs& o, const int* ocs, int64_t i0, cudaStream_t s) {
+    using T = K3Tile<W>;
+    const bool far = MODE == 0 && (a.parts & FFTPIM_FAR);
+    const size_t nf = far ? (size_t)a.fo.n[0] * a.fo.n[1] * a.fo.n[2] : 0;
+    const size_t smem = (T::NODES + nf) * sizeof(cplx) + (2 * T::ROWS + 1) * sizeof(int);
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_observers_tile<W, WF, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    const int tsx0 = a.kx0, tnx = std::min(a.knx, a.g.nc[0] - a.kx0);
+    if (tnx <= 0) return;
+    const int gz = (a.g.nc[2] + K3T_TZ - 1) / K3T_TZ, gy = (a.g.nc[1] + K3T_TY - 1) / K3T_TY;
+    const int gx = (tnx + K3T_TX - 1) / K3T_TX;
+    k_observers_tile<W, WF, MODE><<<gx * gy * gz, K3T_NT, smem, s>>>(a, o, ocs, i0, tsx0, tnx);
+}
+
+template <int W, int MODE>
+static bool obs_tile_far(const EvalArgs& a, const ObsPosArgs& o, const int* ocs, int64_t i0, cudaStream_t s) {
+    switch (a.fo.order + 1) {
+        case 3: obs_tile_launch<W, 3, MODE>(a, o, ocs, i0, s); return true;
+        case 4: obs_tile_launch<W, 4, MODE>(a, o, ocs, i0, s); return true;
+        case 5: obs_tile_launch<W, 5, MODE>(a, o, ocs, i0, s); return true;
+        default: return false;
+    }
+}
+
+template <int MODE>
+static bool obs_tile_near(const EvalArgs& a, const ObsPosArgs& o, const int* ocs, int64_t i0, cudaStream_t s) {
+    switch (a.g.order + 1) {
+        case 3: return obs_tile_far<3, MODE>(a, o, ocs, i0, s);
+        case 4: return obs_tile_far<4, MODE>(a, o, ocs, i0, s);
+        case 5: return obs_tile_far<5, MODE>(a, o, ocs, i0, s);
+        case 6: return obs_tile_far<6, MODE>(a, o, ocs, i0, s);
+        default: return false;
+    }
+}
+
+// mode 0 (fused) and 2 (near + obs_pre) on grid tiles; false: not applicable
+// (mode 1, single-plane axes, orders outside the instantiated set)
+bool launch_observers_tile(const EvalArgs& a, const double* pos, const int* ocs, int64_t i0, cudaStream_t s,
+                           int mode) {
+    if (mode == 1 || !ocs) return false;
+    if (a.g.n[0] < 2 || a.g.n[1] < 2 || a.g.n[2] < 2) return false;
+    if (a.M == 0) return true;
+    ObsPosArgs o;
+    o.pos = pos;
+    for (int ax = 0; ax < 3; ++ax) {
+        o.rn[ax] = a.g.h[ax] > 0 ? 1.0 / a.g.h[ax] : 0.0;
+        o.rf[ax] = a.fo.h[ax] > 0 ? 1.0 / a.fo.h[ax] : 0.0;
+    }
+    const bool ok = mode == 2 ? obs_tile_near<2>(a, o, ocs, i0, s) : obs_tile_near<0>(a, o, ocs, i0, s);
+    if (ok) fftpim_count_launch();
+    return ok;
+}
+
+// ------------------------------------------------------------- K5a on windows
+// Far projection (farzone.py:156, grids.py:167-181 on the 10^3 far source grid)
+// from the sorted positions.  A warp takes a chunk of consecutive sorted points;
+// their far stencil starts span few far cells (the points are sorted by near
+// cell), so the warp first finds the bounding window of its chunk's far nodes
+// and accumulates into a private copy of just that window in shared memory
+// (lane l owns taps l, l + 32, ... and sums runs of points with the same start in
+// registers, flushing on a start change).  A chunk whose window exceeds the
+// shared capacity accumulates straight into its own global slot (private, L2).
+// The chunk windows are then summed per far node in a fixed order
+// (k_far_windows_reduce): no atomics, bitwise reproducible.
+#define FPW_WARPS 8
+#define FPW_CAP 400
+struct FarWinArgs {
+    const double* pos;          // sorted positions of the projected points
+    const cplx* q;              // their sorted charges
+    int64_t n;                  // points
+    int chunk;                  // points per warp chunk
+    int nchunks;
+    cplx* slots;                // (nchunks, nf) windows
+    int* win;                   // (nchunks, 6): x0, y0, z0, ex, ey, ez
+    double rf[3];
+};
+
+template <int WF>
+__global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, FarWinArgs f) {
+    constexpr int TPL = (WF * WF * WF + 31) / 32;
+    constexpr int REC = 3 * WF + 2;
+    extern __shared__ double fpw_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * FPW_WARPS + warp;
+    if (c >= f.nchunks) return;
+    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * FPW_CAP;
+    double* stage = fpw_smem + 2 * FPW_WARPS * FPW_CAP + warp * 32 * REC;
+    int* sst = reinterpret_cast<int*>(fpw_smem + 2 * FPW_WARPS * FPW_CAP + FPW_WARPS * 32 * REC) + warp * 32 * 3;
+    const StencilGeom& fs = a.fs;
+    const int nfx = fs.n[0], nfy = fs.n[1], nfz = fs.n[2];
+    const int nf = nfx * nfy * nfz;
+    const int64_t p0 = (int64_t)c * f.chunk, p1 = min(p0 + f.chunk, f.n);
+    const LagrangeDen<WF> L;
+    // pass 1: bounding window of the chunk's far stencil starts
+    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-1, -1, -1};
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            double w[WF];
+            const int s = fast_stencil<WF>(__ldg(f.pos + 3 * p + ax), fs.n[ax], fs.origin[ax], fs.h[ax], f.rf[ax], L, w);
+            lo[ax] = min(lo[ax], s);
+            hi[ax] = max(hi[ax], s);
+        }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax)
+        for (int o = 16; o; o >>= 1) {
+            lo[ax] = min(lo[ax], __shfl_xor_sync(0xffffffffu, lo[ax], o));
+            hi[ax] = max(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], o));
+        }
+    int ext[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) ext[ax] = min(hi[ax] + fs.w[ax], fs.n[ax]) - lo[ax];
+    const int wn = ext[0] * ext[1] * ext[2];
+    const bool in_smem = wn <= FPW_CAP;
+    cplx* dst = in_smem ? wgrid : f.slots + (int64_t)c * nf;
+    for (int t = lane; t < wn; t += 32) dst[t] = mk(0.0);
+    if (lane < 3) {
+        f.win[6 * c + lane] = lo[lane];
+        f.win[6 * c + 3 + lane] = ext[lane];
+    }
+    // this lane's taps (taps past a single-plane axis are skipped)
+    int ta[TPL], tb[TPL], tc[TPL];
+    bool tok[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) {
+        const int tp = lane + 32 * t;
+        tc[t] = tp % WF;
+        tb[t] = (tp / WF) % WF;
+        ta[t] = tp / (WF * WF);
+        tok[t] = tp < WF * WF * WF && ta[t] < fs.w[0] && tb[t] < fs.w[1] && tc[t] < fs.w[2];
+    }
+    double accr[TPL], acci[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) accr[t] = acci[t] = 0.0;
+    int c0 = -1, c1 = 0, c2 = 0;
+    auto flush = [&]() {
+#pragma unroll
+        for (int t = 0; t < TPL; ++t) {
+            if (!tok[t]) continue;
+            cplx& d = dst[((c0 - lo[0] + ta[t]) * ext[1] + (c1 - lo[1] + tb[t])) * ext[2] + (c2 - lo[2] + tc[t])];
+            d.re += accr[t];
+            d.im += acci[t];
+            accr[t] = acci[t] = 0.0;
+        }
+        __syncwarp();
+    };
+    __syncwarp();
+    // pass 2: batches of 32 points, stencils computed by the loading lane
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int64_t p = base + lane;
+        __syncwarp();
+        if (p < p1) {
+            double* r = stage + lane * REC;
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax)
+                sst[lane * 3 + ax] =
+                    fast_stencil<WF>(__ldg(f.pos + 3 * p + ax), fs.n[ax], fs.origin[ax], fs.h[ax], f.rf[ax], L, r + ax * WF);
+            const double2 qv = __ldg(reinterpret_cast<const double2*>(f.q + p));
+            r[3 * WF] = qv.x;
+            r[3 * WF + 1] = qv.y;
+        }
+        __syncwarp();
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        for (int j = 0; j < cnt; ++j) {
+            const double* r = stage + j * REC;
+            const int s0 = sst[3 * j], s1 = sst[3 * j + 1], s2 = sst[3 * j + 2];
+            if (s0 != c0 || s1 != c1 || s2 != c2) {   // warp-uniform
+                if (c0 >= 0) flush();
+                c0 = s0;
+                c1 = s1;
+                c2 = s2;
+            }
+            const double qre = r[3 * WF], qim = r[3 * WF + 1];
+#pragma unroll
+            for (int t = 0; t < TPL; ++t) {
+                const double wgt = (r[ta[t]] * r[WF + tb[t]]) * r[2 * WF + tc[t]];
+                accr[t] += wgt * qre;
+                acci[t] += wgt * qim;
+            }
+        }
+    }
+    if (c0 >= 0) flush();
+    if (in_smem) {
+        cplx* out = f.slots + (int64_t)c * nf;
+        for (int t = lane; t < wn; t += 32) out[t] = wgrid[t];
+    }
+}
+
+// far node t: sum of the chunk windows covering it, chunks in a fixed tree order
+__global__ void __launch_bounds__(256) k_far_windows_reduce(FarWinArgs f, int nfx, int nfy, int nfz, cplx* qg) {
+    const int t = blockIdx.x;
+    const int x = t / (nfy * nfz), y = (t / nfz) % nfy, z = t % nfz;
+    const int nf = nfx * nfy * nfz;
+    cplx s = mk(0.0);
+    for (int c = threadIdx.x; c < f.nchunks; c += blockDim.x) {
+        const int* w = f.win + 6 * c;
+        const int lx = x - w[0], ly = y - w[1], lz = z - w[2];
+        if (lx >= 0 && lx < w[3] && ly >= 0 && ly < w[4] && lz >= 0 && lz < w[5])
+            s = s + f.slots[(int64_t)c * nf + (lx * w[4] + ly) * w[5] + lz];
+    }
+    __shared__ cplx red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) qg[t] = red[0];
+}
+
+int far_win_chunk(int64_t n) {
+    int64_t c = n / (148 * 16);
+    c = std::max<int64_t>(256, std::min<int64_t>(2048, c));
+    return (int)((c + 31) / 32 * 32);
+}
+
+bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, int* win, cudaStream_t s) {
+    if (!pos || !slots) return false;
+    FarWinArgs f;
+    f.pos = pos;
+    f.q = a.far_q;
+    f.n = a.far_n;
+    f.chunk = far_win_chunk(a.far_n);
+    f.nchunks = (int)((a.far_n + f.chunk - 1) / f.chunk);
+    f.slots = slots;
+    f.win = win;
+    for (int ax = 0; ax < 3; ++ax) f.rf[ax] = a.fs.h[ax] > 0 ? 1.0 / a.fs.h[ax] : 0.0;
+    const int WF = a.fs.order + 1;
+    const size_t smem = (size_t)FPW_WARPS * (FPW_CAP * sizeof(cplx) + 32 * (3 * WF + 2) * sizeof(double) +
+                                             32 * 3 * sizeof(int));
+    const int blocks = (f.nchunks + FPW_WARPS - 1) / FPW_WARPS;
+    auto go = [&](auto kern) {
+        static size_t configured = 48 * 1024;
+        if (smem > configured) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured = smem;
+        }
+        if (f.nchunks > 0) kern<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
+    };
+    switch (WF) {
+        case 3: go(k_far_project_win<3>); break;
+        case 4: go(k_far_project_win<4>); break;
+        case 5: go(k_far_project_win<5>); break;
+        default: return false;
+    }
+    const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
+    k_far_windows_reduce<<<nf, 256, 0, s>>>(f, a.fs.n[0], a.fs.n[1], a.fs.n[2], a.far_qg);
+    fftpim_count_launch(2);
+    return true;
 }

@@ -130,6 +130,8 @@ struct FftpimPlan {
     double* src_rec = nullptr;    // (N, (3W+2)&~1) stencil records for the thread-independent line sweep
     double* obs_pos_s = nullptr;  // (M, 3) observer positions, sorted (aliases src_pos_s if same points)
     bool obs_pos_pass = false;    // observer pass computes its stencils from obs_pos_s
+    bool obs_tile = false;        // ... and gathers the near grid from shared-memory tiles
+    int* obs_cell_start = nullptr;   // observer cell CSR (aliases cell_start if same points)
     double* src_fw = nullptr;     // (N, 3, Wf) far source-grid weights
     int* src_fstart = nullptr;
     double* obs_fw = nullptr;     // far observer-grid weights
@@ -181,6 +183,8 @@ struct FftpimPlan {
     cplx* far_kernel = nullptr;   // (2nf-1)^3
     cplx* far_qg = nullptr;       // projected far source grid
     cplx* far_partial = nullptr;  // per-block partial grids
+    cplx* far_slots = nullptr;    // windowed far projection (line_kernels.cu): per-chunk windows
+    int* far_win = nullptr;
     cplx* far_ug = nullptr;       // far observer-grid potentials
     cplx* obs_pre = nullptr;      // split observer pass: far + K4 fix-up (concurrent schedule)
     int far_blocks_seq = 0;            // far projection grid for sequential chains

@@ -53,6 +53,15 @@ def main():
                                    kshift=(0.3, 0.1, 0), regime=fp.Regime("dynamic"))
         box, obs = fp.TargetBox((1, 1, 0.25)), pos
         prm = fp.SolverParams(near_grid=(48, 192, 12), near_order=3, far_grid=(6, 6, 4))
+    elif case == "g256":
+        # 256^3 grid: L = 512 on every axis (z, y forward stages, fused x stage, inverses)
+        rng = np.random.default_rng(256)
+        pos = rng.uniform(0.0, 1.0, (20000, 3))
+        q = rng.standard_normal(20000) + 1j * rng.standard_normal(20000)
+        cfg = fp.PeriodicityConfig(dim=fp.Periodicity(3), L=(1, 1, 1), k0=2.0 * np.pi,
+                                   kshift=(0.2 * np.pi, 0.1 * np.pi, 0), regime=fp.Regime("dynamic"))
+        box, obs = fp.TargetBox((1, 1, 1)), pos
+        prm = fp.SolverParams(near_grid=(256, 256, 256), near_order=3, far_grid=(6, 6, 6))
     else:
         from cases import SMALL_CASES, case_inputs, regime_of
         d = SMALL_CASES[case]

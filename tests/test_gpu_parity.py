@@ -69,13 +69,14 @@ def test_small_case_parity(fp, name):
     assert rel_l2(fp.eval_far(plan.far, q), g["u_far"]) <= TOL
 
 
-@pytest.mark.parametrize("k1", ["lines", "lines_smem"])
+@pytest.mark.parametrize("k1,obs,far", [("lines", "pos", "warps"), ("lines_smem", "tile", "win")])
 @pytest.mark.parametrize("name", list(SMALL_CASES))
-def test_small_case_parity_point_paths(fp, name, k1, monkeypatch):
+def test_small_case_parity_point_paths(fp, name, k1, obs, far, monkeypatch):
     """The large-N evaluation paths forced on every small case: K1 as a line
     sweep (line_kernels.cu: plan stencil records, or stencils computed from the
     sorted positions) and the observer pass computing its stencils from the
-    sorted positions.  Same potentials as the reference (1e-10) and as the
+    sorted positions (gathering from global memory, or from shared-memory grid
+    tiles), and the far projection on per-chunk windows.  Same potentials as the reference (1e-10) and as the
     default small-N paths (ELL K1, stored-weight observer pass) to 1e-13."""
     case = SMALL_CASES[name]
     g = golden(f"small_{name}.npz")
@@ -86,7 +87,8 @@ def test_small_case_parity_point_paths(fp, name, k1, monkeypatch):
         warnings.simplefilter("ignore")
         base = fp.build_plan(cfg, box, src, ob, prm)
         monkeypatch.setenv("FFTPIM_K1", k1)
-        monkeypatch.setenv("FFTPIM_OBS", "pos")
+        monkeypatch.setenv("FFTPIM_OBS", obs)
+        monkeypatch.setenv("FFTPIM_FAR", far)
         plan = fp.build_plan(cfg, box, src, ob, prm)
     u = plan.evaluate(q)
     assert rel_l2(u, g["u"]) <= TOL

@@ -5,8 +5,8 @@ same plan geometry):
   tap-major / line-sweep) projections -- the ELL rows keep the gather order and
   weight expression, so the potentials agree to rounding of the exact-zero
   padding; the line sweep sums in another fixed order (1e-13);
-* K2: the register-resident column FFTs vs the shared-memory Stockham stages
-  vs cuFFT;
+* K2: the register-resident column FFTs (incl. L = 512 as 8 x 8 x 8 and as
+  32 x 16) vs the shared-memory Stockham stages vs cuFFT;
 * the host entry with pinned buffers (one graph: upload, evaluation,
   download) vs pageable buffers vs the device entry;
 * misaligned device buffers are rejected with FFTPIM_VALUE.
@@ -55,9 +55,12 @@ def test_k1_ell_matches_computed_projection(case, tmp_path):
         assert rel_l2(u_ell, u_tap) <= 1e-13
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d", "tri"])
+@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d", "tri", "g256"])
 def test_register_fft_matches_stockham_and_cufft(case, tmp_path):
     u_reg, _ = run_variant(case, {}, tmp_path, "reg")
+    if case == "g256":   # L = 512: the 8 x 8 x 8 kernel vs the E = 32 two-level one
+        u_e32, _ = run_variant(case, {"FFTPIM_FFT_R8": "0"}, tmp_path, "e32")
+        assert rel_l2(u_reg, u_e32) <= 1e-13
     u_smem, _ = run_variant(case, {"FFTPIM_FFT_REG": "0"}, tmp_path, "smem")
     if case == "tri":   # the radix-3 register kernels alone switched off
         u_r3, _ = run_variant(case, {"FFTPIM_FFT_REG3": "0"}, tmp_path, "noreg3")
