@@ -283,6 +283,14 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * w.n_points / float(te.item())
+    # the stock drop-in call: plan.evaluate(q_numpy) with pageable buffers and a
+    # fresh output array per call (what a reference user writes, solver.py:24-25)
+    n_pg = max(2, min(args.steps, 10))
+    plan.evaluate(q)
+    t0 = time.perf_counter()
+    for _ in range(n_pg):
+        plan.evaluate(q)
+    e2e_pageable = world * w.n_points / ((time.perf_counter() - t0) / n_pg)
 
     # parity of this very run against the reference's own output (C1/C2 full,
     # C3/C4/C5 on the reference's seeded observer sample)
@@ -324,7 +332,9 @@ def run_b200(args):
                          "chains in order (K4 uses the whole chip)"),
             "stage_gbs": {k: nbytes[k] / (prof[k] * 1e-3) / 1e9 for k in nbytes if prof.get(k, 0) > 0},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * w.n_points,
-                    "d2h_bytes_per_step": 16 * w.n_points},
+                    "d2h_bytes_per_step": 16 * w.n_points, "buffers": "pinned host (evaluate(q, out=u))"},
+            "e2e_pageable": {"value": e2e_pageable, "unit": UNIT, "calls": n_pg,
+                             "buffers": "pageable numpy, fresh output per call (plan.evaluate(q))"},
             "gpu_launches": int(launches),
             "build_seconds": build_s,
             "clocks": clocks.summary(),

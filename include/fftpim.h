@@ -68,6 +68,12 @@ typedef struct FftpimProblem {
     const double* obs_pos;      /* (n_obs, 3) row-major, HOST memory; NULL = same as src */
     int32_t same_points;        /* 1: observers are the sources (nearzone.py:241-243) */
     int32_t device;             /* CUDA device ordinal */
+    int32_t parts;              /* zones to build: FFTPIM_ALL (0 = ALL), FFTPIM_NEAR = build_near_plan
+                                   (nearzone.py:194-273), FFTPIM_FAR = build_far_plan (farzone.py:76-131) */
+    int32_t reserved_;
+    const double* far_kernel;   /* HOST (2nf-1)^3 complex128 far-kernel table read from a PIMF blob, or
+                                   NULL: tabulate it (farzone.py:103-123: a cache hit skips pgf_far_many) */
+    int64_t far_kernel_terms;   /* the blob's kernel_terms (used with far_kernel) */
 } FftpimProblem;
 
 /* Summary read by the reference CLI (cli.py:232-236) and by the tests. */
@@ -91,6 +97,10 @@ typedef struct FftpimInfo {
     int32_t k1_operator;        /* 1: projection held as the plan-time sliced-ELL operator */
     int32_t custom_fft;         /* 1: pruned column-FFT stages, 0: cuFFT full transforms */
     int64_t k1_slots;           /* sliced-ELL entries including padding */
+    int32_t built_parts;        /* FFTPIM_NEAR | FFTPIM_FAR zones this plan can evaluate */
+    int32_t reserved_;
+    int64_t graph_captures;     /* evaluation graphs captured (caller buffers changed) */
+    int64_t graph_instantiations;   /* of those, executables instantiated (the rest updated in place) */
 } FftpimInfo;
 
 typedef struct FftpimPlan FftpimPlan;

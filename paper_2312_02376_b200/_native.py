@@ -31,6 +31,8 @@ class Problem(C.Structure):
         ("n_src", C.c_int64), ("n_obs", C.c_int64),
         ("src_pos", C.c_void_p), ("obs_pos", C.c_void_p),
         ("same_points", C.c_int32), ("device", C.c_int32),
+        ("parts", C.c_int32), ("reserved_", C.c_int32),
+        ("far_kernel", C.c_void_p), ("far_kernel_terms", C.c_int64),
     ]
 
 
@@ -44,6 +46,8 @@ class Info(C.Structure):
         ("device_bytes", C.c_int64), ("build_seconds", C.c_double),
         ("real_coefficients", C.c_int32), ("k1_operator", C.c_int32), ("custom_fft", C.c_int32),
         ("k1_slots", C.c_int64),
+        ("built_parts", C.c_int32), ("reserved_", C.c_int32),
+        ("graph_captures", C.c_int64), ("graph_instantiations", C.c_int64),
     ]
 
 

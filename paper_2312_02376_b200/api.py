@@ -51,8 +51,12 @@ def _same_points(src: SourcePointSet, obs: ObserverPointSet) -> bool:
 
 
 def problem_struct(cfg: PeriodicityConfig, box: TargetBox, src: SourcePointSet, obs: ObserverPointSet,
-                   params: SolverParams, device: int | None = None):
-    """FftpimProblem for the C ABI; returns (struct, same_points, arrays to keep alive)."""
+                   params: SolverParams, device: int | None = None, parts: int = nat.ALL, far_kernel=None,
+                   far_kernel_terms: int = 0):
+    """FftpimProblem for the C ABI; returns (struct, same_points, arrays to keep alive).
+    `parts` selects the zones to build (build_near_plan / build_far_plan build one,
+    nearzone.py:194-273, farzone.py:76-131); `far_kernel` is a far-kernel table read
+    from a PIMF blob, used instead of tabulating the series (farzone.py:103-112)."""
     same = _same_points(src, obs)
     pr = nat.Problem()
     pr.dim = cfg.dim.value
@@ -79,47 +83,32 @@ def problem_struct(cfg: PeriodicityConfig, box: TargetBox, src: SourcePointSet, 
     pr.obs_pos = None if same else op.ctypes.data
     pr.same_points = int(same)
     pr.device = _default_device() if device is None else int(device)
-    return pr, same, (sp, op)
+    pr.parts = int(parts)
+    keep = [sp, op]
+    if far_kernel is not None:
+        fk = np.ascontiguousarray(far_kernel, dtype=np.complex128)
+        keep.append(fk)
+        pr.far_kernel = fk.ctypes.data
+        pr.far_kernel_terms = int(far_kernel_terms)
+    return pr, same, tuple(keep)
 
 
 class NativePlan:
     """Owns one libfftpim plan (device memory lives until this object dies)."""
 
     def __init__(self, cfg: PeriodicityConfig, box: TargetBox, src: SourcePointSet,
-                 obs: ObserverPointSet, params: SolverParams, device: int | None = None):
+                 obs: ObserverPointSet, params: SolverParams, device: int | None = None,
+                 parts: int = nat.ALL, far_kernel=None, far_kernel_terms: int = 0):
         lib = nat.load()
         self.cfg, self.box, self.params = cfg, box, params
-        same = _same_points(src, obs)
-        pr = nat.Problem()
-        pr.dim = cfg.dim.value
-        pr.regime = REGIME_CODE[cfg.regime]
-        for a in range(3):
-            pr.L[a] = cfg.L[a]
-            pr.D[a] = box.D[a]
-            pr.kshift[a][0] = cfg.kshift[a].real
-            pr.kshift[a][1] = cfg.kshift[a].imag
-            pr.far_grid[a] = params.far_grid[a]
-        pr.k0[0], pr.k0[1] = cfg.k0.real, cfg.k0.imag
-        pr.i_d = params.i_d
-        pr.near_order = params.near_order
-        dims = params.resolve_near_grid(max(len(src), len(obs)), box)
-        for a in range(3):
-            pr.near_grid[a] = int(dims[a])
-        pr.far_order = params.far_order
-        pr.series_tol = params.series_tol
-        pr.er_range_boxes = params.er_range_boxes
-        self._src_pos = np.ascontiguousarray(src.positions, dtype=np.float64)
-        self._obs_pos = self._src_pos if same else np.ascontiguousarray(obs.positions, dtype=np.float64)
-        pr.n_src, pr.n_obs = len(src), len(obs)
-        pr.src_pos = self._src_pos.ctypes.data
-        pr.obs_pos = None if same else self._obs_pos.ctypes.data
-        pr.same_points = int(same)
-        pr.device = _default_device() if device is None else int(device)
+        pr, same, keep = problem_struct(cfg, box, src, obs, params, device, parts, far_kernel, far_kernel_terms)
+        self._src_pos, self._obs_pos = keep[0], keep[1]
         self.device = pr.device
         handle = C.c_void_p()
         self._lib = lib
         self._h = None
         nat.check(lib.fftpim_plan_create(C.byref(pr), C.byref(handle)))
+        del keep
         self._h = handle
         info = nat.Info()
         nat.check(lib.fftpim_plan_info(self._h, C.byref(info)))
@@ -195,6 +184,11 @@ class NativePlan:
             raise ValueError(f"unknown operand {which}")
         nat.check(self._lib.fftpim_plan_export(self._h, which, out.ctypes.data, out.nbytes))
         return out
+
+    def refresh_info(self):
+        """Re-read the plan summary (graph capture counters change with use)."""
+        nat.check(self._lib.fftpim_plan_info(self._h, C.byref(self.info)))
+        return self.info
 
     def set_far_kernel(self, kernel: np.ndarray):
         k = np.ascontiguousarray(kernel, dtype=np.complex128)
@@ -306,23 +300,34 @@ class SolveResult:
     eval_seconds: float
 
 
-def _validated_native(cfg, box, src, obs, params, device=None) -> NativePlan:
+def _validated_native(cfg, box, src, obs, params, device=None, parts=nat.ALL, kernel_cache=None) -> NativePlan:
     params = params or SolverParams()
     report = validate_problem(cfg, box, src, obs, params)
     if report:
         raise ValidationError(report)
-    return NativePlan(cfg, box, src, obs, params, device)
+    if kernel_cache is None or not (parts & nat.FAR):
+        return NativePlan(cfg, box, src, obs, params, device, parts)
+    return _native_with_kernel_cache(cfg, box, src, obs, params, device, parts, kernel_cache)
+
+
+def _check_provider(provider):
+    """The reference threads a SpectralTransformProvider (nearzone.py:29-48) into
+    the near-zone FFT; the B200 plan runs its pruned column FFTs on the device and
+    has no host transform to replace -- refuse rather than silently ignore it."""
+    if provider is not None:
+        raise TypeError("the B200 plan transforms on the device: a SpectralTransformProvider "
+                        f"({type(provider).__name__}) cannot be plugged in; pass provider=None")
 
 
 def build_plan(cfg: PeriodicityConfig, box: TargetBox, src: SourcePointSet, obs: ObserverPointSet,
                params: SolverParams | None = None, provider=None, kernel_cache=None,
                device: int | None = None) -> SolvePlan:
-    """solver.py:35-45.  `provider` is accepted for signature compatibility; the
-    B200 plan always transforms with cuFFT on the device."""
+    """solver.py:35-45.  `kernel_cache`: PIMF far-kernel blob path (a hit skips the
+    far series, a miss tabulates and writes it, farzone.py:103-123).  `provider` must
+    be None (see _check_provider)."""
+    _check_provider(provider)
     t0 = time.perf_counter()
-    native = _validated_native(cfg, box, src, obs, params, device)
-    if kernel_cache is not None:
-        _apply_kernel_cache(native, kernel_cache)
+    native = _validated_native(cfg, box, src, obs, params, device, nat.ALL, kernel_cache)
     return SolvePlan(NearZonePlan(native), FarZonePlan(native), time.perf_counter() - t0)
 
 
@@ -335,31 +340,35 @@ def solve(cfg, box, src, obs, params=None, provider=None, kernel_cache=None) -> 
 
 
 def build_near_plan(cfg, box, src, obs, params, provider=None) -> NearZonePlan:
-    """nearzone.py:194-197 signature; validation follows the facade's rules.
-    i_d = 0 builds a near-zone-only plan (free-space near kernel, no wrapped
-    copies, nearzone.py:205-212, :314), as the reference's bench baseline does
+    """nearzone.py:194-197 signature; builds the near zone only (no far series,
+    no far buffers).  Validation follows the facade's rules; i_d = 0 builds a
+    near-zone-only plan (free-space near kernel, no wrapped copies,
+    nearzone.py:205-212, :314), as the reference's bench baseline does
     (cli.py:343-347); the far-zone and D_ER rules only apply for i_d >= 1."""
+    _check_provider(provider)
     params = params or SolverParams()
     if params.i_d != 0:
-        return NearZonePlan(_validated_native(cfg, box, src, obs, params))
+        return NearZonePlan(_validated_native(cfg, box, src, obs, params, parts=nat.NEAR))
     report = validate_problem(cfg, box, src, obs, params)
     rest = tuple(m for m in report.messages if "i_d must be" not in m and "error-correction range" not in m)
     if rest:
         raise ValidationError(type(report)(rest))
-    return NearZonePlan(NativePlan(cfg, box, src, obs, params))
+    return NearZonePlan(NativePlan(cfg, box, src, obs, params, parts=nat.NEAR))
 
 
 def eval_near(plan: NearZonePlan, q, provider=None):
     """nearzone.py:490-525: project, FFT convolve, interpolate, correct."""
+    _check_provider(provider)
     return plan.native.evaluate(q, nat.NEAR)
 
 
 def build_far_plan(cfg, box, src, obs, params, cache_path=None) -> FarZonePlan:
-    """farzone.py:76-131 signature."""
-    native = _validated_native(cfg, box, src, obs, params)
-    if cache_path is not None:
-        _apply_kernel_cache(native, cache_path)
-    return FarZonePlan(native)
+    """farzone.py:76-131: the far zone only (no correction pairs, no near FFT
+    operands); `cache_path` is the PIMF kernel blob (hit: table and kernel_terms
+    from the blob, no series; miss: tabulate and save)."""
+    if params is not None and params.i_d < 1:
+        raise ValueError("far-zone engine requires i_d >= 1")
+    return FarZonePlan(_validated_native(cfg, box, src, obs, params, parts=nat.FAR, kernel_cache=cache_path))
 
 
 def eval_far(plan: FarZonePlan, q):
@@ -419,14 +428,23 @@ def load_far_kernel(path, expect_dims=None, expect_regime=None, expect_signature
     return arr.reshape(shape).copy(), int(terms)
 
 
-def _apply_kernel_cache(native: NativePlan, path):
-    """Blob hit: replace the freshly tabulated table; miss: export it (farzone.py:103-123)."""
-    far = FarZonePlan(native)
-    dims = far.source_grid.dims
-    sig = _kernel_signature(native.cfg, native.box, dims, native.params.i_d, native.params.series_tol)
+def _far_dims(params: SolverParams, box: TargetBox):
+    return tuple(params.far_grid[a] if box.D[a] > 0.0 else 1 for a in range(3))
+
+
+def _native_with_kernel_cache(cfg, box, src, obs, params, device, parts, path) -> NativePlan:
+    """farzone.py:103-123: a blob matching this problem (dims, regime, signature)
+    supplies the far kernel and kernel_terms and the series is skipped; on a miss
+    (no file, or any KernelCacheError) the plan tabulates the kernel and the blob
+    is (re)written."""
+    dims = _far_dims(params, box)
+    sig = _kernel_signature(cfg, box, dims, params.i_d, params.series_tol)
     try:
-        kernel, _ = load_far_kernel(path, expect_dims=dims, expect_regime=native.cfg.regime,
-                                    expect_signature=sig)
-        native.set_far_kernel(kernel)
+        kernel, terms = load_far_kernel(path, expect_dims=dims, expect_regime=cfg.regime, expect_signature=sig)
     except (FileNotFoundError, KernelCacheError):
-        save_far_kernel(far, path)
+        kernel, terms = None, 0
+    native = NativePlan(cfg, box, src, obs, params, device, parts, far_kernel=kernel, far_kernel_terms=terms)
+    native.kernel_cache_hit = kernel is not None
+    if kernel is None:
+        save_far_kernel(FarZonePlan(native), path)
+    return native

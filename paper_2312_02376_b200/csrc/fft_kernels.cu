@@ -797,9 +797,9 @@ static bool launch_fft_stage_reg(const FftStage& st, cudaStream_t s) {
         const char* e = getenv("FFTPIM_FFT_REG3");
         return !(e && e[0] == '0');
     }();
-    static const bool r8 = [] {   // L = 512 as 8 x 8 x 8 (FFTPIM_FFT_R8=0: the E = 32 two-level kernel)
-        const char* e = getenv("FFTPIM_FFT_R8");
-        return !(e && e[0] == '0');
+    static const bool r8 = [] {   // L = 512 as 8 x 8 x 8: FFTPIM_FFT_R8=1 (measured 2x slower at C4 than
+        const char* e = getenv("FFTPIM_FFT_R8");   // the E = 32 two-level kernel: shared-memory bound)
+        return e && e[0] == '1';
     }();
     return reg_launch<64>(st, s) || reg_launch<128>(st, s) || reg_launch<256>(st, s) ||
            (r512 && r8 && r8x3_launch(st, s)) || (r512 && reg_launch<512>(st, s)) ||

@@ -523,6 +523,22 @@ static int64_t concurrent_max_pairs() {
     return v;
 }
 
+// largest observer count of a grid-tile observer-pass tile (line_kernels.cu),
+// from the observer cell CSR (built here when observers are not the sources)
+int64_t max_tile_count(FftpimPlan* P, const int* ocs, const double* d_obs, int64_t M, cudaStream_t s) {
+    int* tmp = nullptr;
+    if (!ocs) {
+        int* perm = dalloc<int>(P, M);
+        tmp = dalloc<int>(P, prod3(P->near_g.nc) + 1);
+        sort_points(P, d_obs, M, perm, tmp, s);
+        dfree(P, perm);
+        ocs = tmp;
+    }
+    const int64_t v = launch_max_tile_count(P->near_g, ocs, s);
+    if (tmp) dfree(P, tmp);
+    return v;
+}
+
 void build(FftpimPlan* P) {
     const FftpimProblem& pr = P->prob;
     cudaStream_t s = P->build_stream;
@@ -541,6 +557,14 @@ void build(FftpimPlan* P) {
         pr.far_order > FFTPIM_MAX_ORDER)
         throw Fail{FFTPIM_VALUE, "interpolation order must be in [1, 6]"};
     if (pr.i_d > 2) throw Fail{FFTPIM_VALUE, "i_d > 2 is not supported by this build"};
+    // zones to build: build_near_plan / build_far_plan build only their half
+    const int bparts = pr.parts ? pr.parts : FFTPIM_ALL;
+    if (bparts & ~FFTPIM_ALL) throw Fail{FFTPIM_VALUE, "parts must be a non-empty subset of NEAR|FAR"};
+    if (bparts != FFTPIM_ALL && (P->sweep || P->sharded))
+        throw Fail{FFTPIM_VALUE, "sweep and slab plans build both zones"};
+    if (P->near_only && bparts == FFTPIM_FAR) throw Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"};
+    P->info.built_parts = P->near_only ? FFTPIM_NEAR : bparts;
+    const bool want_near = bparts & FFTPIM_NEAR, want_far = (bparts & FFTPIM_FAR) && !P->near_only;
 
     // ---- near grid (nearzone.py:198-211, grids.py:90-107)
     int dims[3];
@@ -639,7 +663,11 @@ void build(FftpimPlan* P) {
         // FFTPIM_K1=lines|ell|gather|taps overrides
         const char* e = getenv("FFTPIM_K1");
         const bool ok = W >= 3 && W <= 6;
-        const std::string mode = e ? e : "ell";
+        // measured (B200): the line sweep wins on sparse grids (C4, 0.5 points per
+        // stencil cell: 1.5 vs 2.9 ms), the ELL operator on denser ones (C5 1.3 per
+        // cell: 0.37 vs 0.86 ms; clustered C3: 1.7 vs 6.9 ms)
+        const double density = (double)N / (double)prod3(P->near_g.nc);
+        const std::string mode = e ? e : (N > 262144 && density < 0.75 ? "lines_smem" : "ell");
         P->k1_lines = ok && (mode == "lines" || mode == "lines_smem");
         if (P->k1_lines && mode == "lines_smem") {
             P->src_pos_s = dalloc<double>(P, 3 * N);
@@ -670,8 +698,14 @@ void build(FftpimPlan* P) {
     {
         // observer pass with stencils from sorted positions (line_kernels.cu) for
         // large observer sets; FFTPIM_OBS=pos|weights overrides
+        // measured: the grid-tile pass wins for large, evenly spread observer sets
+        // (C4 1.7 vs 2.5 ms, C5 0.25 vs 0.33 ms); clustered sets (C3 blobs: a few
+        // tiles hold thousands of observers) keep the stored-weight pass
         const char* e = getenv("FFTPIM_OBS");
-        const std::string om = e ? e : "weights";
+        std::string om = e ? e : "weights";
+        if (!e && M > 262144 && dims[0] > 1 && dims[1] > 1 && dims[2] > 1 &&
+            max_tile_count(P, same ? P->cell_start : nullptr, d_obs, M, s) <= 2048)
+            om = "tile";
         P->obs_pos_pass = W >= 3 && W <= 6 && WF >= 3 && WF <= 5 && (om == "pos" || om == "tile");
         P->obs_tile = P->obs_pos_pass && om == "tile";
         if (P->obs_tile) {
@@ -727,10 +761,11 @@ void build(FftpimPlan* P) {
     const int64_t Mown = P->i1 - P->i0;
 
     // ---- near kernel table -> kernel_hat (nearzone.py:215-235)
-    P->khat = dalloc<cplx>(P, P->n_fft);
     unsigned long long* d_cnt = dalloc<unsigned long long>(P, 4);
     CK(cudaMemsetAsync(d_cnt, 0, 4 * sizeof(unsigned long long), s));
     launch_count_coincident(dims, h, im, d_cnt, s);
+    if (want_near) {
+    P->khat = dalloc<cplx>(P, P->n_fft);
     {
         int rank = 0, n[3];
         for (int a = 0; a < 3; ++a)
@@ -746,6 +781,7 @@ void build(FftpimPlan* P) {
         P->pad_in = dalloc<cplx>(P, P->n_fft);
         CK(cudaMemsetAsync(P->pad_in, 0, sizeof(cplx) * P->n_fft, s));   // padding stays zero: out-of-place forward FFT
     }
+    }   // want_near
     P->q_sorted = dalloc<cplx>(P, N);
     {
         // tap-major K1 (3 active axes, orders 2..4) pays off for crowded cells
@@ -923,7 +959,10 @@ void build(FftpimPlan* P) {
     pa.d0min = d0mm;
     pa.d0max = d0mm + 81;
     pa.tallies = d_cnt + 1;
-    launch_pairs_count(pg, pa, s);
+    if (want_near)
+        launch_pairs_count(pg, pa, s);
+    else   // far-zone-only plan: no correction pairs
+        CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (Mown + 1), s));
     check_status(P, "correction pair discovery");
     P->pair_ptr = dalloc<int64_t>(P, Mown + 1);
     {
@@ -1034,7 +1073,7 @@ void build(FftpimPlan* P) {
     // half the free memory; FFTPIM_K1=gather|taps|ell overrides
     {
         const char* e = getenv("FFTPIM_K1");
-        if (!P->k1_lines && (!e || std::string(e) == "ell")) {
+        if (want_near && !P->k1_lines && (!e || std::string(e) == "ell")) {
             EvalArgs a = eval_args(P, nullptr, nullptr, FFTPIM_NEAR);
             const int64_t rows = (int64_t)a.knx * dims[1] * dims[2];
             const int64_t nsl = (rows + 31) / 32;
@@ -1114,10 +1153,17 @@ void build(FftpimPlan* P) {
 
     // ---- far kernel (farzone.py:100-121, pgf.py:450-462)
     P->far_kernel = dalloc<cplx>(P, prod3(P->far_kdims));
-    if (P->near_only)
+    if (!want_far) {
         CK(cudaMemsetAsync(P->far_kernel, 0, sizeof(cplx) * prod3(P->far_kdims), s));
-    else
+    } else if (pr.far_kernel) {
+        // kernel blob hit (farzone.py:103-112): the table and its kernel_terms come
+        // from the blob, the series is not evaluated
+        CK(cudaMemcpyAsync(P->far_kernel, pr.far_kernel, sizeof(cplx) * prod3(P->far_kdims),
+                           cudaMemcpyHostToDevice, s));
+        P->info.kernel_terms = pr.far_kernel_terms;
+    } else {
         P->info.kernel_terms = tabulate_far(P, pr.kshift, im, P->far_kernel, s);
+    }
     // ---- sweep: kernel_hat and far kernel per excitation
     if (P->sweep) {
         const int64_t nk = prod3(P->far_kdims);
@@ -1186,7 +1232,7 @@ void build(FftpimPlan* P) {
         {
             // windowed far projection from the sorted positions (FFTPIM_FAR=win|warps)
             const char* e = getenv("FFTPIM_FAR");
-            const bool win = (e ? std::string(e) == "win" : false) && pr.far_order + 1 >= 3 && pr.far_order + 1 <= 5;
+            const bool win = (e ? std::string(e) == "win" : N > 262144) && pr.far_order + 1 >= 3 && pr.far_order + 1 <= 5;
             if (win) {
                 if (!P->src_pos_s) {
                     P->src_pos_s = dalloc<double>(P, 3 * N);
@@ -1554,6 +1600,10 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
 void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int parts, cudaStream_t s,
               cudaEvent_t* ev = nullptr) {
     if (parts & ~FFTPIM_ALL || parts == 0) throw Fail{FFTPIM_VALUE, "parts must be a non-empty subset of NEAR|FAR"};
+    if (parts & ~P->info.built_parts)
+        throw Fail{FFTPIM_VALUE, (parts & FFTPIM_NEAR) && !(P->info.built_parts & FFTPIM_NEAR)
+                                     ? "plan was built without the near zone (build_far_plan)"
+                                     : "plan was built without the far zone (build_near_plan)"};
     CK(cudaSetDevice(P->device));
     if (!ev) ensure_batch_buffers(P, batch, parts);
     if (!ev && P->use_graphs) {
@@ -1568,8 +1618,13 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
             s = P->gstream;
         }
         if (!(P->graph_exec && P->g_q == q && P->g_u == u && P->g_batch == batch && P->g_parts == parts)) {
-            if (P->graph_exec) cudaGraphExecDestroy(P->graph_exec);
-            P->graph_exec = nullptr;
+            // same batch and parts, new caller buffers: capture again and update the
+            // executable in place (no re-instantiation); otherwise instantiate anew
+            const bool updatable = P->graph_exec && P->g_batch == batch && P->g_parts == parts;
+            if (P->graph_exec && !updatable) {
+                cudaGraphExecDestroy(P->graph_exec);
+                P->graph_exec = nullptr;
+            }
             cudaGraph_t graph = nullptr;
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             P->capturing = true;
@@ -1585,7 +1640,21 @@ void evaluate(FftpimPlan* P, const double* q, double* u, int64_t batch, int part
             }
             P->capturing = false;
             CK(cudaStreamEndCapture(s, &graph));
-            CK(cudaGraphInstantiate(&P->graph_exec, graph, 0));
+            ++P->info.graph_captures;
+            bool updated = false;
+            if (P->graph_exec) {
+                cudaGraphExecUpdateResultInfo res{};
+                updated = cudaGraphExecUpdate(P->graph_exec, graph, &res) == cudaSuccess;
+                if (!updated) {
+                    cudaGetLastError();
+                    cudaGraphExecDestroy(P->graph_exec);
+                    P->graph_exec = nullptr;
+                }
+            }
+            if (!updated) {
+                CK(cudaGraphInstantiate(&P->graph_exec, graph, 0));
+                ++P->info.graph_instantiations;
+            }
             CK(cudaGraphDestroy(graph));
             P->g_q = q;
             P->g_u = u;
@@ -1893,6 +1962,7 @@ static int plan_create_shard(const FftpimProblem* p, int world, int rank, bool s
         build(P);
         P->prob.src_pos = nullptr;
         P->prob.obs_pos = nullptr;
+        P->prob.far_kernel = nullptr;
         P->info.device_bytes = P->device_bytes;
         P->info.build_seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -1097,3 +1097,34 @@ bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, i
     fftpim_count_launch(2);
     return true;
 }
+
+// observers per K3 tile (TX x TY x TZ stencil-start cells), max over tiles
+__global__ void k_max_tile_count(StencilGeom g, const int* __restrict__ ocs, int* out) {
+    const int gz = (g.nc[2] + K3T_TZ - 1) / K3T_TZ, gy = (g.nc[1] + K3T_TY - 1) / K3T_TY;
+    const int gx = (g.nc[0] + K3T_TX - 1) / K3T_TX;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)gx * gy * gz) return;
+    const int bz = (int)(t % gz), by = (int)((t / gz) % gy), bx = (int)(t / ((int64_t)gz * gy));
+    int n = 0;
+    for (int r = 0; r < K3T_TX * K3T_TY; ++r) {
+        const int sx = bx * K3T_TX + r / K3T_TY, sy = by * K3T_TY + r % K3T_TY;
+        if (sx >= g.nc[0] || sy >= g.nc[1]) continue;
+        const int64_t k = ((int64_t)sx * g.nc[1] + sy) * g.nc[2];
+        n += ocs[k + min((bz + 1) * K3T_TZ, g.nc[2])] - ocs[k + bz * K3T_TZ];
+    }
+    atomicMax(out, n);
+}
+int64_t launch_max_tile_count(const StencilGeom& g, const int* ocs, cudaStream_t s) {
+    int* d = nullptr;
+    cudaMallocAsync(&d, sizeof(int), s);
+    cudaMemsetAsync(d, 0, sizeof(int), s);
+    const int64_t tiles = (int64_t)((g.nc[0] + K3T_TX - 1) / K3T_TX) * ((g.nc[1] + K3T_TY - 1) / K3T_TY) *
+                          ((g.nc[2] + K3T_TZ - 1) / K3T_TZ);
+    k_max_tile_count<<<(int)((tiles + 255) / 256), 256, 0, s>>>(g, ocs, d);
+    int h = 0;
+    cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(d, s);
+    fftpim_count_launch();
+    return h;
+}
