@@ -12,9 +12,10 @@ far kernel are used; only the observer set is sampled.
 
     python tests/golden/make_subset_golden.py 3 5      # ~10 min each, ~9 GB RAM
     python tests/golden/make_subset_golden.py 4        # ~15 min, ~60 GB RAM
+    python tests/golden/make_subset_golden.py 5:31 5:63   # C5 excitations 31 and 63
 
-Writes tests/golden/c<c>_subset.npz: observer indices, u at those observers,
-pair counts and the far kernel table.
+Writes tests/golden/c<c>_subset.npz (C5 excitation e > 0: c5_subset_e<e>.npz):
+observer indices, u at those observers, pair counts and the far kernel table.
 """
 from __future__ import annotations
 
@@ -57,13 +58,14 @@ def main(configs):
     P, tmp = patched_reference()
     import perisum.nearzone as NZ
     try:
-        for c in configs:
+        for spec in configs:
+            c, e = (int(v) for v in spec.split(":")) if ":" in spec else (int(spec), 0)
             w = CONFIGS[c]
             pos, q = make_inputs(c)
             kshift = w.kshift
             if c == 5:
-                q = q[0]
-                kshift = c5_kshift(0)
+                q = q[e]
+                kshift = c5_kshift(e)
             idx = np.sort(np.random.default_rng(100 + c).choice(len(pos), SUBSET[c], replace=False))
             NZ._OBS_TO_SRC = idx
             cfg = P.PeriodicityConfig(dim=P.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=kshift,
@@ -78,7 +80,8 @@ def main(configs):
             u = plan.evaluate(q)
             te = time.perf_counter() - t0
             n = plan.near
-            np.savez_compressed(os.path.join(HERE, f"c{c}_subset.npz"), obs_index=idx, u=u,
+            name = f"c{c}_subset.npz" if e == 0 else f"c{c}_subset_e{e}.npz"
+            np.savez_compressed(os.path.join(HERE, name), obs_index=idx, u=u, excitation=np.int64(e),
                                 n_pairs=np.int64(n.pair_obs.size), n_self=np.int64(n.n_self_pairs),
                                 n_wrap=np.int64(n.n_wrapped_pairs), far_kernel=plan.far.kernel,
                                 far_terms=np.int64(plan.far.kernel_terms), kshift=np.array(kshift),
@@ -90,4 +93,4 @@ def main(configs):
 
 
 if __name__ == "__main__":
-    main([int(v) for v in sys.argv[1:]] or [3, 5])
+    main(sys.argv[1:] or ["3", "5"])

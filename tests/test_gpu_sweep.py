@@ -73,13 +73,15 @@ def test_sweep_errors(fp):
 
 
 def test_sweep_c5_subset(fp):
-    """C5 at full scale: four excitations in one sweep; excitation 0 against the
-    reference's sample, two others against independent plans."""
+    """C5 at full scale: five excitations in one sweep; excitations 0, 31 and 63
+    against the reference's own runs on the seeded observer sample
+    (tests/golden/make_subset_golden.py 5 5:31 5:63), two against independent
+    plans."""
     from paper_2312_02376_b200.workloads import CONFIGS, c5_kshift, make_inputs
     g = golden("c5_subset.npz")
     w = CONFIGS[5]
     pos, qall = make_inputs(5)
-    es = [0, 17, 40, 63]
+    es = [0, 17, 31, 40, 63]
     Q = np.ascontiguousarray(qall[es])
     cfg = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=c5_kshift(0),
                                regime=fp.Regime(w.regime))
@@ -88,6 +90,10 @@ def test_sweep_c5_subset(fp):
     U = sw.evaluate(Q)
     sel = g["obs_index"]
     assert rel_l2(U[0][sel], g["u"]) <= 1e-10
+    for j, e in ((2, 31), (4, 63)):
+        ge = golden(f"c5_subset_e{e}.npz")
+        assert int(ge["excitation"]) == e
+        assert rel_l2(U[j][ge["obs_index"]], ge["u"]) <= 1e-10
     del sw
     for j in (1, 3):
         cfg_e = fp.PeriodicityConfig(dim=fp.Periodicity(w.dim), L=w.L, k0=w.k0, kshift=c5_kshift(es[j]),
