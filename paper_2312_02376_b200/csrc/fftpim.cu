@@ -1741,10 +1741,37 @@ struct GroupImpl {
     bool emulate = true;
     std::vector<FftpimPlan*> shards;   // emulate: all shards; NCCL: this rank's shard
     ncclComm_t comm = nullptr;
+    // the whole shard evaluation (streams, NCCL calls) captured once as a CUDA
+    // graph and replayed; re-captured when the caller's buffers change
+    cudaGraphExec_t graph_exec = nullptr;
+    const double* g_q = nullptr;
+    double* g_u = nullptr;
+    cudaStream_t g_stream = nullptr;   // capture stream for legacy-default-stream callers
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    int kernels_per_eval = 0;
 };
+
+// the shard's K4 (its own observers' correction pairs) needs only the permuted
+// charges: it runs on the plan's low-priority stream from right after the
+// permutation, overlapping K1, the FFT stages, both transposes and the halo
+// exchange; the observer pass joins it.  The grid is capped (FFTPIM_CORR_BLOCKS,
+// as in the single-plan concurrent schedule) so the near chain and the NCCL
+// kernels still get SMs.
+static void shard_fork_k4(FftpimPlan* P, EvalArgs a, cudaStream_t s) {
+    static const int cap = [] {
+        const char* e = getenv("FFTPIM_SLAB_CORR_BLOCKS");
+        return e ? atoi(e) : 222;
+    }();
+    a.corr_blocks = cap;
+    CK(cudaEventRecord(P->ev_fork, s));
+    CK(cudaStreamWaitEvent(P->aux[1], P->ev_fork, 0));
+    launch_corr_tiles(a, P->aux[1]);
+    CK(cudaEventRecord(P->ev_join[1], P->aux[1]));
+}
 
 void shard_phase1(FftpimPlan* P, const EvalArgs& a, cudaStream_t s) {
     launch_permute_q(a, s);
+    shard_fork_k4(P, a, s);
     launch_near_project(a, s);
     launch_fft_stage(P->stage[0], s);
     launch_fft_stage(P->stage[1], s);
@@ -1775,7 +1802,7 @@ void shard_phase3(FftpimPlan* P, const EvalArgs& a, cudaStream_t s) {
     launch_far_sum(a, s);
 }
 
-void group_evaluate(GroupImpl* G, const double* q, double* u, cudaStream_t s) {
+void group_schedule(GroupImpl* G, const double* q, double* u, cudaStream_t s) {
     const int W = G->world;
     std::vector<EvalArgs> args;
     for (auto* P : G->shards) {
@@ -1867,10 +1894,67 @@ void group_evaluate(GroupImpl* G, const double* q, double* u, cudaStream_t s) {
         NCK(ncclGroupEnd());
     }
     for (int k = 0; k < ns; ++k) {
-        launch_corr_tiles(args[k], s);
+        CK(cudaStreamWaitEvent(s, G->shards[k]->ev_join[1], 0));   // the shard's K4
         launch_observers(args[k], s);
     }
     CK(cudaGetLastError());
+}
+
+void group_evaluate(GroupImpl* G, const double* q, double* u, cudaStream_t s) {
+    FftpimPlan* P0 = G->shards[0];
+    CK(cudaSetDevice(P0->device));
+    if (!P0->use_graphs) {
+        group_schedule(G, q, u, s);
+        return;
+    }
+    if (!G->g_stream) {
+        CK(cudaStreamCreateWithFlags(&G->g_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&G->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&G->ev_out, cudaEventDisableTiming));
+    }
+    const cudaStream_t caller = s;
+    if (caller == nullptr) {   // the legacy default stream cannot be captured
+        CK(cudaEventRecord(G->ev_in, caller));
+        CK(cudaStreamWaitEvent(G->g_stream, G->ev_in, 0));
+        s = G->g_stream;
+    }
+    if (!(G->graph_exec && G->g_q == q && G->g_u == u)) {
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        for (auto* P : G->shards) P->capturing = true;
+        const long long l0 = g_launches.load();
+        try {
+            group_schedule(G, q, u, s);
+        } catch (...) {
+            for (auto* P : G->shards) P->capturing = false;
+            cudaStreamEndCapture(s, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        for (auto* P : G->shards) P->capturing = false;
+        G->kernels_per_eval = (int)(g_launches.load() - l0);
+        CK(cudaStreamEndCapture(s, &graph));
+        bool updated = false;
+        if (G->graph_exec) {
+            cudaGraphExecUpdateResultInfo res{};
+            updated = cudaGraphExecUpdate(G->graph_exec, graph, &res) == cudaSuccess;
+            if (!updated) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(G->graph_exec);
+                G->graph_exec = nullptr;
+            }
+        }
+        if (!updated) CK(cudaGraphInstantiate(&G->graph_exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        G->g_q = q;
+        G->g_u = u;
+    }
+    CK(cudaGraphLaunch(G->graph_exec, s));
+    fftpim_count_launch(G->kernels_per_eval);
+    if (caller == nullptr) {
+        CK(cudaEventRecord(G->ev_out, s));
+        CK(cudaStreamWaitEvent(caller, G->ev_out, 0));
+    }
 }
 
 // Orders an evaluation after the plan's previous one when the caller switches
@@ -2375,6 +2459,10 @@ int fftpim_group_info(const FftpimGroup* g, int32_t shard, FftpimInfo* info) {
 void fftpim_group_destroy(FftpimGroup* g) {
     GroupImpl* G = reinterpret_cast<GroupImpl*>(g);
     if (!G) return;
+    if (G->graph_exec) cudaGraphExecDestroy(G->graph_exec);
+    if (G->g_stream) cudaStreamDestroy(G->g_stream);
+    if (G->ev_in) cudaEventDestroy(G->ev_in);
+    if (G->ev_out) cudaEventDestroy(G->ev_out);
     for (auto* P : G->shards) fftpim_plan_destroy(P);
     if (G->comm) ncclCommDestroy(G->comm);
     delete G;

@@ -54,6 +54,27 @@ def test_slab_group_dynamic_3d_small(fp):
         assert rel_l2(SlabGroup(*args, world=world).evaluate(q), u1) <= 1e-13
 
 
+def test_slab_group_w8_helmholtz_64_order4(fp):
+    """The C4 regime (3D Helmholtz, phase shift, order 4) on a 64^3 grid over 8
+    emulated shards -- the G = 8 decomposition of the SCALE run -- against the
+    single-domain plan; repeated evaluations replay one captured graph (K4 on
+    its own stream beside the transposes) and stay bitwise identical."""
+    from paper_2312_02376_b200.sharding import SlabGroup
+    rng = np.random.default_rng(64)
+    n = 120000
+    pos = rng.uniform(0, 1, (n, 3))
+    q = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity.P3D, L=(1, 1, 1), k0=2 * np.pi,
+                               kshift=(0.2 * np.pi, 0.1 * np.pi, 0), regime=fp.Regime.DYNAMIC)
+    prm = fp.SolverParams(near_grid=(64, 64, 64), near_order=4)
+    args = (cfg, fp.TargetBox((1, 1, 1)), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos), prm)
+    u1 = fp.build_plan(*args).evaluate(q)
+    grp = SlabGroup(*args, world=8)
+    u = grp.evaluate(q)
+    assert rel_l2(u, u1) <= 1e-13
+    np.testing.assert_array_equal(grp.evaluate(q), u)
+
+
 @pytest.mark.parametrize("c", [1, 2])
 def test_slab_group_nccl_single_rank(fp, c):
     """The NCCL code path itself (send/recv transposes, all-reduce, halo) with a
