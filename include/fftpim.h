@@ -101,6 +101,10 @@ typedef struct FftpimInfo {
     int32_t reserved_;
     int64_t graph_captures;     /* evaluation graphs captured (caller buffers changed) */
     int64_t graph_instantiations;   /* of those, executables instantiated (the rest updated in place) */
+    int64_t k4_wide_groups;     /* 32-pair groups whose source indices need 32 bits (-1: 16-bit offsets off) */
+    int32_t pair_rows_source_order;   /* 1: each observer's pairs are stored (and exported) in source order,
+                                         0: in the reference's discovery order (nearzone.py:374-478) */
+    int32_t reserved2_;
 } FftpimInfo;
 
 typedef struct FftpimPlan FftpimPlan;

@@ -48,6 +48,8 @@ class Info(C.Structure):
         ("k1_slots", C.c_int64),
         ("built_parts", C.c_int32), ("reserved_", C.c_int32),
         ("graph_captures", C.c_int64), ("graph_instantiations", C.c_int64),
+        ("k4_wide_groups", C.c_int64),
+        ("pair_rows_source_order", C.c_int32), ("reserved2_", C.c_int32),
     ]
 
 

@@ -14,6 +14,9 @@
 // The observer pass adds the <= 1 + P/M/256 segments of its row in order.
 // No atomics, fixed orders: bitwise reproducible.
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <climits>
+#include <vector>
 
 #include "geom.cuh"
 #include "kernels.h"
@@ -284,6 +287,322 @@ __global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles(EvalA
     }
 }
 
+// ------------------------------------------------------------- K4, 16-bit indices
+// The source index stream is 4 of the 20 (complex) or 12 (NPSP) bytes a pair
+// costs.  Pairs are grouped by 32 (the K4 load groups); a group whose source
+// indices span <= 65535 stores them as 16-bit offsets from a per-group int32
+// base (grp_base >= 0), a wider group (observer-row or wrapped-copy transitions)
+// is marked grp_base < 0 and reads the full int32 indices.  The group bases
+// travel with the tile's row-start words one tile ahead of the stream, so the
+// stream loads of a tile (16-bit offsets or int32 indices, coefficients) never
+// wait on them.  Same pairs, same order, same arithmetic: the potentials are
+// bit-identical to the int32 path.
+struct CorrMeta {
+    int gb;            // lane k < 8: base of the tile's group k (< 0: wide)
+    unsigned word;     // lane k < 8: row-start bits of group k
+    int64_t sbase;
+};
+
+__device__ __forceinline__ void corr_meta(const EvalArgs& a, int64_t t, int lane, CorrMeta& m) {
+    const int64_t g0 = t * (CORR_TILE / 32);
+    m.gb = lane < 8 ? __ldcs(a.grp_base + g0 + lane) : 0;
+    m.word = lane < 8 ? a.head_bits[g0 + lane] : 0u;
+    m.sbase = a.seg_base[t];
+}
+
+template <bool REAL>
+__device__ __forceinline__ void corr_stream(const EvalArgs& a, int64_t t, int lane, const CorrMeta& m,
+                                            CorrTile& d) {
+    const int64_t T0 = t * CORR_TILE;
+    const int valid = (int)min((int64_t)CORR_TILE, a.n_pairs - T0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int e = 32 * k + lane;
+        const bool ok = e < valid;
+        const int gb = __shfl_sync(0xffffffffu, m.gb, k);
+        if (gb >= 0)
+            d.src[k] = ok ? (int)__ldcs(a.pair_off16 + T0 + e) : 0;
+        else
+            d.src[k] = ok ? __ldcs(a.pair_src + T0 + e) : 0;
+        if (REAL) {
+            d.cr[k] = ok ? __ldcs(a.coef_r + T0 + e) : 0.0;
+            d.ci[k] = 0.0;
+        } else {
+            const double2 c = ok ? __ldcs(reinterpret_cast<const double2*>(a.coef) + T0 + e) : make_double2(0.0, 0.0);
+            d.cr[k] = c.x;
+            d.ci[k] = c.y;
+        }
+    }
+    d.word = m.word;
+    d.sbase = m.sbase;
+}
+
+// 16-bit offsets -> sorted source indices (lane k < 8 of gbw holds group k's base)
+__device__ __forceinline__ void corr_decode(int* src, int gbw) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int gb = __shfl_sync(0xffffffffu, gbw, k);
+        if (gb >= 0) src[k] += gb;
+    }
+}
+
+// NPSP real charges: the three-stage pipeline of corr_tiles_realq (stream of tile
+// t + 2s, gathers of t + s, reduction of t) with the group bases one stage earlier
+__device__ __forceinline__ void corr_stream_real(const EvalArgs& a, int64_t t, int lane, const CorrMeta& m,
+                                                 RealTile& d) {
+    const int64_t T0 = t * CORR_TILE;
+    const int valid = (int)min((int64_t)CORR_TILE, a.n_pairs - T0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int e = 32 * k + lane;
+        const bool ok = e < valid;
+        const int gb = __shfl_sync(0xffffffffu, m.gb, k);
+        if (gb >= 0)
+            d.src[k] = ok ? (int)__ldcs(a.pair_off16 + T0 + e) : 0;
+        else
+            d.src[k] = ok ? __ldcs(a.pair_src + T0 + e) : 0;
+        d.cr[k] = ok ? __ldcs(a.coef_r + T0 + e) : 0.0;
+    }
+    d.word = m.word;
+    d.sbase = m.sbase;
+}
+
+__device__ __forceinline__ void corr_tiles_realq_c16(const EvalArgs& a, int64_t t, int64_t stride, int64_t T,
+                                                     int lane) {
+    const double zero[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    RealTile c0, c1;
+    CorrMeta m0, m1, m2;
+    double q0[8];
+    int g1 = 0;
+    corr_meta(a, t, lane, m0);
+    corr_stream_real(a, t, lane, m0, c0);
+    corr_decode(c0.src, m0.gb);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q0[k] = a.q_re[c0.src[k]];
+    if (t + stride < T) {
+        corr_meta(a, t + stride, lane, m1);
+        corr_stream_real(a, t + stride, lane, m1, c1);
+        g1 = m1.gb;
+    }
+    if (t + 2 * stride < T) corr_meta(a, t + 2 * stride, lane, m2);
+    for (; t < T; t += stride) {
+        CorrMeta m3;
+        if (t + 3 * stride < T) corr_meta(a, t + 3 * stride, lane, m3);
+        RealTile c2;
+        int g2 = 0;
+        if (t + 2 * stride < T) {
+            corr_stream_real(a, t + 2 * stride, lane, m2, c2);
+            g2 = m2.gb;
+        }
+        double q1[8];
+        if (t + stride < T) {
+            corr_decode(c1.src, g1);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q1[k] = a.q_re[c1.src[k]];
+        }
+        corr_reduce_tile(a, lane, c0.cr, zero, q0, zero, c0.word, c0.sbase);
+        c0 = c1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q0[k] = q1[k];
+        c1 = c2;
+        g1 = g2;
+        m2 = m3;
+    }
+}
+
+template <bool REAL>
+__global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_tiles_c16(EvalArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
+    const int64_t stride = (int64_t)gridDim.x * CORR_WARPS;
+    int64_t t = (int64_t)blockIdx.x * CORR_WARPS + warp;
+    if (t >= T) return;
+    const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
+    if (REAL && realq) {
+        corr_tiles_realq_c16(a, t, stride, T, lane);
+        return;
+    }
+    // pipeline: meta of tile t + 2s, stream of tile t + s, gathers + reduction of tile t
+    CorrMeta m1, m2;
+    CorrTile cur, nxt;
+    int gcur, gnxt = 0;
+    {
+        CorrMeta m0;
+        corr_meta(a, t, lane, m0);
+        corr_stream<REAL>(a, t, lane, m0, cur);
+        gcur = m0.gb;
+    }
+    if (t + stride < T) corr_meta(a, t + stride, lane, m1);
+    for (; t < T; t += stride) {
+        if (t + 2 * stride < T) corr_meta(a, t + 2 * stride, lane, m2);
+        if (t + stride < T) {
+            corr_stream<REAL>(a, t + stride, lane, m1, nxt);
+            gnxt = m1.gb;
+        }
+        corr_decode(cur.src, gcur);
+        double qr[8], qi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            cplx qv;
+            if (realq) {
+                qv.re = a.q_re[cur.src[k]];
+                qv.im = 0.0;
+            } else {
+                qv = a.q_sorted[cur.src[k]];
+            }
+            qr[k] = qv.re;
+            qi[k] = qv.im;
+        }
+        corr_reduce_tile(a, lane, cur.cr, cur.ci, qr, qi, cur.word, cur.sbase);
+        cur = nxt;
+        gcur = gnxt;
+        m1 = m2;
+    }
+}
+
+// per 32-pair group: base = smallest source index if the group's indices span
+// <= 65535 (16-bit offsets written), else -1 (the group keeps int32 indices)
+__global__ void k_group_encode(const int* __restrict__ src, int64_t P, int64_t G, int* base, unsigned short* off,
+                               unsigned long long* wide) {
+    const int lane = threadIdx.x & 31;
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (g >= G) return;
+    const int64_t p = g * 32 + lane;
+    const int v = p < P ? src[p] : INT_MAX;
+    int lo = v, hi = p < P ? v : INT_MIN;
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const bool narrow = (int64_t)hi - lo <= 65535;
+    if (p < P) off[p] = narrow ? (unsigned short)(v - lo) : (unsigned short)0;
+    if (lane == 0) {
+        base[g] = narrow ? lo : -1;
+        if (!narrow) atomicAdd(wide, 1ull);
+    }
+}
+
+// base: (G + 8) ints (the last tile's lanes read up to 8 groups past the end)
+int64_t build_group_offsets(const int* src, int64_t P, int* base, unsigned short* off, cudaStream_t s) {
+    const int64_t G = (P + 31) / 32;
+    unsigned long long* d = nullptr;
+    cudaMallocAsync(&d, sizeof(unsigned long long), s);
+    cudaMemsetAsync(d, 0, sizeof(unsigned long long), s);
+    cudaMemsetAsync(base + G, 0, 8 * sizeof(int), s);
+    if (G > 0) k_group_encode<<<nblk64(G * 32, 256), 256, 0, s>>>(src, P, G, base, off, d);
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(d, s);
+    fftpim_count_launch();
+    return (int64_t)h;
+}
+
+// ------------------------------------------------------------- pair rows in source order
+// K4 at C4 is bound by L1 wavefronts, and most of them are the q gathers: in the
+// reference's pair order (box offsets db-major, nearzone.py:374-478) consecutive
+// pairs of a row jump between the 4-8 stencil-cell rows a box straddles, so a
+// warp's 32 gathers touch ~16 lines.  Sorting every row by source index makes
+// consecutive lanes read consecutive charges (one or two lines per z run).  Same
+// pair set, same coefficients; only the order of the row sum changes (~1e-16).
+__global__ void k_chunk_offsets(const int64_t* __restrict__ ptr, int64_t r0, int64_t nseg, int* off, int* iota,
+                                int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i <= nseg) off[i] = (int)(ptr[r0 + i] - ptr[r0]);
+    if (i < n) iota[i] = (int)i;
+}
+template <typename T>
+__global__ void k_permute_rows(const T* __restrict__ src, const int* __restrict__ perm, int64_t n, T* dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* coef, double* coef_r, unsigned char* codeid,
+                    size_t budget, cudaStream_t s) {
+    std::vector<int64_t> hp(M + 1);
+    if (cudaMemcpyAsync(hp.data(), ptr, sizeof(int64_t) * (M + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
+    cudaStreamSynchronize(s);
+    const int64_t P = hp[M];
+    const size_t per = 4 + 4 + 4 + 16 + 1 + 16;   // keys out, iota, perm, coefficient and code copies, cub
+    int64_t CH = std::min<int64_t>((int64_t)1 << 28, (int64_t)(budget / per));
+    if (CH < (int64_t)1 << 20) return false;
+    int *koff = nullptr, *iota = nullptr, *perm = nullptr, *kout = nullptr, *offs = nullptr;
+    void* vtmp = nullptr;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    bool ok = true;
+    auto fail = [&] { ok = false; };
+    if (cudaMallocAsync(&iota, sizeof(int) * CH, s) || cudaMallocAsync(&perm, sizeof(int) * CH, s) ||
+        cudaMallocAsync(&kout, sizeof(int) * CH, s) || cudaMallocAsync(&vtmp, sizeof(cplx) * CH, s))
+        fail();
+    (void)koff;
+    int64_t r0 = 0;
+    while (ok && r0 < M) {
+        // rows [r0, r1) with at most CH pairs (a single longer row is left unsorted)
+        int64_t r1 = r0 + 1;
+        {
+            int64_t lo = r0 + 1, hi = M;
+            while (lo < hi) {   // largest r1 with hp[r1] - hp[r0] <= CH
+                const int64_t mid = (lo + hi + 1) / 2;
+                if (hp[mid] - hp[r0] <= CH) lo = mid; else hi = mid - 1;
+            }
+            r1 = lo;
+        }
+        const int64_t n = hp[r1] - hp[r0], nseg = r1 - r0;
+        if (n > CH || nseg > ((int64_t)1 << 30)) {   // one row longer than a chunk: keep its order
+            r0 = r1;
+            continue;
+        }
+        if (n > 1) {
+            if (cudaMallocAsync(&offs, sizeof(int) * (nseg + 1), s)) {
+                fail();
+                break;
+            }
+            k_chunk_offsets<<<nblk64(std::max(nseg + 1, n), 256), 256, 0, s>>>(ptr, r0, nseg, offs, iota, n);
+            const int64_t p0 = hp[r0];
+            size_t need = 0;
+            cub::DeviceSegmentedSort::StableSortPairs(nullptr, need, pair_src + p0, kout, iota, perm, (int)n, (int)nseg,
+                                                       offs, offs + 1, s);
+            if (need > cub_bytes) {
+                if (cub_tmp) cudaFreeAsync(cub_tmp, s);
+                cub_tmp = nullptr;
+                if (cudaMallocAsync(&cub_tmp, need, s)) {
+                    fail();
+                    break;
+                }
+                cub_bytes = need;
+            }
+            cub::DeviceSegmentedSort::StableSortPairs(cub_tmp, cub_bytes, pair_src + p0, kout, iota, perm, (int)n,
+                                                       (int)nseg, offs, offs + 1, s);
+            cudaMemcpyAsync(pair_src + p0, kout, sizeof(int) * n, cudaMemcpyDeviceToDevice, s);
+            if (coef) {
+                k_permute_rows<cplx><<<nblk64(n, 256), 256, 0, s>>>(coef + p0, perm, n, (cplx*)vtmp);
+                cudaMemcpyAsync(coef + p0, vtmp, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, s);
+            }
+            if (coef_r) {
+                k_permute_rows<double><<<nblk64(n, 256), 256, 0, s>>>(coef_r + p0, perm, n, (double*)vtmp);
+                cudaMemcpyAsync(coef_r + p0, vtmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+            }
+            if (codeid) {
+                k_permute_rows<unsigned char><<<nblk64(n, 256), 256, 0, s>>>(codeid + p0, perm, n,
+                                                                             (unsigned char*)vtmp);
+                cudaMemcpyAsync(codeid + p0, vtmp, n, cudaMemcpyDeviceToDevice, s);
+            }
+            cudaFreeAsync(offs, s);
+            offs = nullptr;
+            fftpim_count_launch(3);
+        }
+        r0 = r1;
+    }
+    if (cub_tmp) cudaFreeAsync(cub_tmp, s);
+    if (iota) cudaFreeAsync(iota, s);
+    if (perm) cudaFreeAsync(perm, s);
+    if (kout) cudaFreeAsync(kout, s);
+    if (vtmp) cudaFreeAsync(vtmp, s);
+    cudaStreamSynchronize(s);
+    return ok && cudaGetLastError() == cudaSuccess;
+}
+
 void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.n_pairs == 0) return;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
@@ -292,6 +611,14 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.corr_blocks > 0) cap = std::min<int64_t>(cap, a.corr_blocks);
     if (a.corr_blocks < 0) cap = INT32_MAX;   // one block per CORR_WARPS tiles (no grid-stride loop)
     const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, cap);
+    if (a.pair_off16) {
+        if (a.coef_r)
+            k_corr_tiles_c16<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        else
+            k_corr_tiles_c16<false><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        fftpim_count_launch();
+        return;
+    }
     // one tile in flight beyond the one being reduced (measured: deeper is not faster)
     if (a.coef_r)
         k_corr_tiles<true, CORR_PF_REAL><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);

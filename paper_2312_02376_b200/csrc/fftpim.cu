@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <thread>
 #include <climits>
 #include <cmath>
 #include <complex>
@@ -1049,6 +1050,41 @@ void build(FftpimPlan* P) {
         launch_pairs_fill(pg, im, tb, pa, s);
     }
     P->n_tiles = (npairs + CORR_TILE - 1) / CORR_TILE;
+    P->info.pair_rows_source_order = 0;
+    if (!P->sweep && npairs > 0) {
+        // rows in source order for large pair lists (K4 gather locality, see
+        // sort_pair_rows); FFTPIM_K4_SORT=0|1 overrides.  Exports then list each
+        // observer's pairs in source order (same set as the reference).
+        const char* e = getenv("FFTPIM_K4_SORT");
+        if (e ? e[0] == '1' : npairs >= (int64_t)1 << 28) {
+            size_t free_b = 0, tot_b = 0;
+            CK(cudaMemGetInfo(&free_b, &tot_b));
+            const size_t budget = (size_t)(0.6 * (double)free_b);
+            if (sort_pair_rows(P->pair_ptr, Mown, P->pair_src, P->pair_coef, P->pair_coef_r, P->pair_codeid, budget, s))
+                P->info.pair_rows_source_order = 1;
+            else
+                cudaGetLastError();
+        }
+    }
+    P->info.k4_wide_groups = -1;
+    if (!P->sweep && npairs > 0) {
+        // 16-bit source offsets for K4 (2 B instead of 4 B per pair) when they fit
+        // in memory; FFTPIM_K4_C16=0|1 overrides (default: large pair lists)
+        const char* e = getenv("FFTPIM_K4_C16");
+        // measured slower at C4 (K4 21.2 -> 28.6 ms: the kernel is bound by L1
+        // wavefronts, not DRAM bytes, and the group decode adds to it): opt-in
+        bool c16 = e ? e[0] == '1' : false;
+        if (c16) {
+            size_t free_b = 0, tot_b = 0;
+            CK(cudaMemGetInfo(&free_b, &tot_b));
+            c16 = (double)npairs * 2.2 < 0.8 * (double)free_b;
+        }
+        if (c16) {
+            P->pair_off16 = dalloc<unsigned short>(P, npairs);
+            P->grp_base = dalloc<int>(P, (npairs + 31) / 32 + 8);
+            P->info.k4_wide_groups = build_group_offsets(P->pair_src, npairs, P->grp_base, P->pair_off16, s);
+        }
+    }
     if (!P->sweep) {   // the batched sweep K4 walks pair_ptr rows directly
         P->head_bits = dalloc<unsigned>(P, (npairs + 31) / 32 + 8);
         P->seg_first = dalloc<int64_t>(P, Mown + 1);
@@ -1307,6 +1343,8 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.n_fft = P->n_fft;
     a.pair_ptr = P->pair_ptr;
     a.pair_src = P->pair_src;
+    a.pair_off16 = P->pair_off16;
+    a.grp_base = P->grp_base;
     a.coef = P->pair_coef;
     a.coef_r = P->pair_coef_r;
     a.q_re = P->q_re;
@@ -2483,6 +2521,77 @@ int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t b
     }
 }
 
+// Pageable caller buffers (the stock plan.evaluate(numpy) call): the bytes go
+// through plan-owned pinned staging buffers in 8 MiB chunks -- host threads copy
+// chunk k into pinned memory while the DMA engine uploads chunk k - 1, and on
+// the way back they copy chunk k out while chunk k + 1 downloads -- instead of
+// the driver's serial pageable copies.
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    static const int nt = [] {
+        const char* e = getenv("FFTPIM_HOST_COPY_THREADS");
+        const int hw = (int)std::thread::hardware_concurrency();
+        return std::max(1, e ? atoi(e) : std::min(8, std::max(1, hw / 2)));
+    }();
+    const int k = (int)std::min<size_t>(nt, std::max<size_t>(1, bytes >> 20));
+    if (k <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (bytes / k + 63) & ~(size_t)63;
+    for (int i = 0; i < k; ++i) {
+        const size_t o = (size_t)i * per;
+        if (o >= bytes) break;
+        const size_t n = std::min(per, bytes - o);
+        th.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, n); });
+    }
+    for (auto& t : th) t.join();
+}
+
+static void staged_host_evaluate(FftpimPlan* P, const double* q, double* u, size_t qb, size_t ub, int64_t batch,
+                                 int parts, cudaStream_t s) {
+    constexpr size_t CH = (size_t)8 << 20;
+    if (P->pin_bytes < std::max(qb, ub)) {
+        if (P->pin_q) cudaFreeHost(P->pin_q);
+        if (P->pin_u) cudaFreeHost(P->pin_u);
+        P->pin_q = P->pin_u = nullptr;
+        CK(cudaMallocHost(&P->pin_q, qb));
+        CK(cudaMallocHost(&P->pin_u, ub));
+        P->pin_bytes = std::max(qb, ub);
+        for (auto& e : P->pin_ev) {
+            if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
+    for (size_t o = 0; o < qb; o += CH) {
+        const size_t n = std::min(CH, qb - o);
+        parallel_memcpy((char*)P->pin_q + o, (const char*)q + o, n);
+        CK(cudaMemcpyAsync((char*)P->h_q + o, (char*)P->pin_q + o, n, cudaMemcpyHostToDevice, s));
+    }
+    evaluate(P, P->h_q, P->h_u, batch, parts, s);
+    // download in chunks, each copied out as soon as its event fires
+    const int nev = (int)(sizeof(P->pin_ev) / sizeof(P->pin_ev[0]));
+    std::vector<size_t> offs;
+    for (size_t o = 0; o < ub; o += CH) offs.push_back(o);
+    size_t done = 0;
+    for (size_t i = 0; i < offs.size(); ++i) {
+        if (i >= (size_t)nev) {   // recycle the event of chunk i - nev
+            const size_t j = i - nev;
+            CK(cudaEventSynchronize(P->pin_ev[j % nev]));
+            const size_t n = std::min(CH, ub - offs[j]);
+            parallel_memcpy((char*)u + offs[j], (char*)P->pin_u + offs[j], n);
+            done = j + 1;
+        }
+        const size_t n = std::min(CH, ub - offs[i]);
+        CK(cudaMemcpyAsync((char*)P->pin_u + offs[i], (char*)P->h_u + offs[i], n, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(P->pin_ev[i % nev], s));
+    }
+    for (size_t j = done; j < offs.size(); ++j) {
+        CK(cudaEventSynchronize(P->pin_ev[j % nev]));
+        const size_t n = std::min(CH, ub - offs[j]);
+        parallel_memcpy((char*)u + offs[j], (char*)P->pin_u + offs[j], n);
+    }
+}
+
 int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts) {
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (plan->near_only && (parts & FFTPIM_FAR)) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
@@ -2549,6 +2658,8 @@ int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int6
             }
             CK(cudaGraphLaunch(P->hgraph_exec, s));
             fftpim_count_launch(P->hkernels_per_eval * (int)batch);
+        } else if (qb + ub >= ((size_t)8 << 20)) {
+            staged_host_evaluate(plan, q, u, qb, ub, batch, parts, s);
         } else {
             CK(cudaMemcpyAsync(plan->h_q, q, qb, cudaMemcpyHostToDevice, s));
             evaluate(plan, plan->h_q, plan->h_u, batch, parts, s);
@@ -2702,6 +2813,10 @@ void fftpim_plan_destroy(FftpimPlan* plan) {
     if (plan->fft_plan) cufftDestroy(plan->fft_plan);
     if (plan->graph_exec) cudaGraphExecDestroy(plan->graph_exec);
     if (plan->hgraph_exec) cudaGraphExecDestroy(plan->hgraph_exec);
+    if (plan->pin_q) cudaFreeHost(plan->pin_q);
+    if (plan->pin_u) cudaFreeHost(plan->pin_u);
+    for (auto& e : plan->pin_ev)
+        if (e) cudaEventDestroy(e);
     for (void* p : plan->allocations) cudaFree(p);
     for (auto st : plan->aux)
         if (st) {

@@ -159,6 +159,8 @@ struct FftpimPlan {
     // corrections (CSR over sorted observers)
     int64_t* pair_ptr = nullptr;  // (M+1)
     int* pair_src = nullptr;      // (P) sorted source index
+    unsigned short* pair_off16 = nullptr;   // (P) 16-bit offsets from the 32-pair group base (K4)
+    int* grp_base = nullptr;      // (P/32 + 8) group bases, -1: the group reads pair_src
     unsigned char* pair_codeid = nullptr;  // (P) code id (export only)
     cplx* pair_coef = nullptr;    // (P) complex coefficients (dynamic / static-shifted)
     double* pair_coef_r = nullptr;  // (P) real coefficients (NPSP)
@@ -205,6 +207,10 @@ struct FftpimPlan {
     double* h_u = nullptr;
     int64_t h_batch = 0;
     cudaGraphExec_t hgraph_exec = nullptr;   // upload + evaluation + download, pinned buffers
+    void* pin_q = nullptr;        // pinned staging for pageable caller buffers (host entry)
+    void* pin_u = nullptr;
+    size_t pin_bytes = 0;
+    cudaEvent_t pin_ev[8] = {};
     const double* hg_q = nullptr;
     double* hg_u = nullptr;
     int64_t hg_batch = 0;

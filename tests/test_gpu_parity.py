@@ -98,6 +98,35 @@ def test_small_case_parity_point_paths(fp, name, k1, obs, far, monkeypatch):
     np.testing.assert_array_equal(plan.evaluate(q), u)   # bitwise reproducible
 
 
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+def test_source_ordered_pair_rows(fp, name, monkeypatch):
+    """Rows stored in source order (the default for large pair lists, K4 gather
+    locality): the same (observer, source, image code, coefficient) set as the
+    reference-order plan, the same potentials to 1e-13, bitwise reproducible."""
+    case = SMALL_CASES[name]
+    pos, q, obs = case_inputs(name)
+    cfg, box, src, ob, prm = ref_objects(fp, case, pos, q, obs)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        base = fp.build_plan(cfg, box, src, ob, prm)
+        monkeypatch.setenv("FFTPIM_K4_SORT", "1")
+        plan = fp.build_plan(cfg, box, src, ob, prm)
+    assert plan.native.info.pair_rows_source_order == 1 and base.native.info.pair_rows_source_order == 0
+
+    def rows(p):
+        n = p.near
+        code = n.pair_code.astype(np.int64)
+        key = np.lexsort((code[:, 2], code[:, 1], code[:, 0], n.pair_src, n.pair_obs))
+        return n.pair_obs[key], n.pair_src[key], n.pair_code[key], n.pair_coef[key]
+
+    for a, b in zip(rows(plan), rows(base)):
+        np.testing.assert_array_equal(a, b)
+    u = plan.evaluate(q)
+    assert rel_l2(u, base.evaluate(q)) <= 1e-13
+    np.testing.assert_array_equal(plan.evaluate(q), u)
+
+
 def _full(fp, c):
     from paper_2312_02376_b200.workloads import CONFIGS, make_inputs
     w = CONFIGS[c]

@@ -71,6 +71,40 @@ def test_register_fft_matches_stockham_and_cufft(case, tmp_path):
     assert rel_l2(u_reg, u_cufft) <= 1e-13
 
 
+@pytest.mark.parametrize("case", ["c1", "c2", "blobs3d"])
+def test_k4_16bit_offsets_bitwise(case, tmp_path):
+    """K4 with 16-bit source offsets per 32-pair group (int32 for wide groups):
+    same pairs, order and arithmetic as the int32 stream -> identical bits."""
+    u16, _ = run_variant(case, {"FFTPIM_K4_C16": "1"}, tmp_path, "c16")
+    u32, _ = run_variant(case, {"FFTPIM_K4_C16": "0"}, tmp_path, "c32")
+    np.testing.assert_array_equal(u16, u32)
+
+
+def test_pageable_host_entry_staged():
+    """Pageable caller buffers above 8 MiB go through the plan's pinned staging in
+    chunks (host threads copying beside the DMA): bitwise equal to the device
+    entry and to pinned buffers."""
+    import torch
+    import paper_2312_02376_b200 as fp
+    rng = np.random.default_rng(300)
+    n = 300_000
+    pos = rng.uniform(0.0, 1.0, (n, 3))
+    q = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(3), L=(1, 1, 1), k0=2.0 * np.pi,
+                               kshift=(0.2 * np.pi, 0.1 * np.pi, 0), regime=fp.Regime("dynamic"))
+    plan = fp.build_plan(cfg, fp.TargetBox((1, 1, 1)), fp.SourcePointSet(pos, q), fp.ObserverPointSet(pos),
+                         fp.SolverParams(near_grid=(64, 64, 64), near_order=3, far_grid=(6, 6, 6)))
+    u_page = plan.evaluate(q)                                     # pageable in, fresh pageable out
+    u_page2 = plan.evaluate(q[::-1].copy()[::-1].copy())          # another pageable buffer
+    u_dev = plan.evaluate(torch.from_numpy(q).cuda()).cpu().numpy()
+    q_pin = torch.from_numpy(q).pin_memory()
+    u_pin = torch.empty(n, dtype=torch.complex128).pin_memory()
+    plan.native.evaluate(q_pin.numpy(), out=u_pin.numpy())
+    np.testing.assert_array_equal(u_page, u_dev)
+    np.testing.assert_array_equal(u_page2, u_dev)
+    np.testing.assert_array_equal(u_pin.numpy(), u_dev)
+
+
 def test_host_entries_and_alignment():
     import torch
     import paper_2312_02376_b200 as fp

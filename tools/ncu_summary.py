@@ -1,7 +1,8 @@
 """Summaries of the round's ncu outputs for profiles/.
 
     python tools/ncu_summary.py launches <launches.csv>      # per-kernel launch list
-    python tools/ncu_summary.py full <full.ncu-rep> <json>   # --set full digest + traffic json
+    python tools/ncu_summary.py full <full.ncu-rep> <json> [label] [source]
+        # --set full digest; merges {label: per-stage DRAM bytes} into <json>
 
 `launches`: the --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --csv list of one bench command, aggregated per kernel
@@ -20,8 +21,9 @@ from collections import defaultdict
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "us": 1.0, "ms": 1e3, "usecond": 1.0,
          "msecond": 1e3, "second": 1e6}
 
-STAGE_OF = {"k_corr_tiles": "corr_matvec", "k_k1_spmv": "near_project", "k_observers": "observers",
-            "k_far_project": "far_project", "k_permute_q": "permute_q", "k_far_sum": "far_sum"}
+STAGE_OF = {"k_corr_tiles": "corr_matvec", "k_k1_spmv": "near_project", "k_k1_lines": "near_project",
+            "k_observers": "observers", "k_far_project": "far_project", "k_permute_q": "permute_q",
+            "k_far_sum": "far_sum"}
 
 
 def launches(path):
@@ -57,13 +59,13 @@ RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "launch__grid_size", "launch__block_size"]
 
 
-def full(rep, js):
+def full(rep, js, label="C2", source=None):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
     iK = h.index("Kernel Name")
     traffic = {}
-    print("# ncu --set full, C2 (bench.py --steps 2 --warmup 3 --no-cpu-baseline, FFTPIM_NO_GRAPHS=1)")
+    print(f"# ncu --set full, {label} (bench.py --steps 2 --warmup 3 --no-cpu-baseline, FFTPIM_NO_GRAPHS=1)")
     print("# per launch: time us | DRAM MB (read+write) | DRAM % of peak | warps active % | regs | "
           "inst | L2 hit % | L1 % | issue % | grid x block | top stalls")
     for v in rows[2:]:
@@ -86,12 +88,20 @@ def full(rep, js):
         for pre, stage in STAGE_OF.items():
             if name.startswith(pre) and stage not in traffic:
                 traffic[stage] = int(b)
-    json.dump({"C2": traffic, "source": "profiles/r01_c2_ncu_full.txt (dram__bytes_read.sum + "
-               "dram__bytes_write.sum per launch, first launch of each stage kernel)"}, open(js, "w"), indent=1)
+    try:
+        doc = json.load(open(js))
+    except (OSError, ValueError):
+        doc = {}
+    doc[label] = traffic
+    doc.setdefault("sources", {})[label] = source or rep
+    doc["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, first launch of each stage kernel "
+                   "in the --set full capture named in sources")
+    doc.pop("source", None)
+    json.dump(doc, open(js, "w"), indent=1)
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
-        full(sys.argv[2], sys.argv[3])
+        full(sys.argv[2], sys.argv[3], *sys.argv[4:6])
