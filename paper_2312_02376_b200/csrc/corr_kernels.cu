@@ -517,8 +517,8 @@ __global__ void k_permute_rows(const T* __restrict__ src, const int* __restrict_
     if (i < n) dst[i] = src[perm[i]];
 }
 
-bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* coef, double* coef_r, unsigned char* codeid,
-                    size_t budget, cudaStream_t s) {
+bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* const* carr, int ncarr, double* coef_r,
+                    unsigned char* codeid, size_t budget, cudaStream_t s) {
     std::vector<int64_t> hp(M + 1);
     if (cudaMemcpyAsync(hp.data(), ptr, sizeof(int64_t) * (M + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
     cudaStreamSynchronize(s);
@@ -575,7 +575,8 @@ bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* coef, do
             cub::DeviceSegmentedSort::StableSortPairs(cub_tmp, cub_bytes, pair_src + p0, kout, iota, perm, (int)n,
                                                        (int)nseg, offs, offs + 1, s);
             cudaMemcpyAsync(pair_src + p0, kout, sizeof(int) * n, cudaMemcpyDeviceToDevice, s);
-            if (coef) {
+            for (int c = 0; c < ncarr; ++c) {   // coefficients (or the sweep's phase components)
+                cplx* coef = carr[c];
                 k_permute_rows<cplx><<<nblk64(n, 256), 256, 0, s>>>(coef + p0, perm, n, (cplx*)vtmp);
                 cudaMemcpyAsync(coef + p0, vtmp, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, s);
             }

@@ -396,6 +396,49 @@ __device__ __forceinline__ void dft_reg(cplx (&a)[N]) {
     }
 }
 
+// In-place radix-2 decimation in frequency on a register array (N | 32), then a
+// compile-time bit-reversal renaming: natural order in and out.  Each butterfly
+// overwrites its own two inputs, so the live set stays ~N values (the Stockham
+// passes above keep input and output arrays live together); FFTPIM_FFT_IP=1
+// selects it for the L = 512 (E = 32) register kernel.
+template <int N>
+__host__ __device__ constexpr int bitrev_c(int k) {
+    int r = 0;
+    for (int m = 1; m < N; m <<= 1) {
+        r = (r << 1) | (k & 1);
+        k >>= 1;
+    }
+    return r;
+}
+template <int N, int SIGN>
+__device__ __forceinline__ void dft_reg_ip(cplx (&a)[N]) {
+#pragma unroll
+    for (int h = N / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int b = 0; b < N; b += 2 * h) {
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const cplx u = a[b + j], v = a[b + j + h];
+                a[b + j] = u + v;
+                const cplx d = u - v;
+                // w_{2h}^j = w_32^(j * 16 / h)
+                const int e = j * (16 / h);
+                if (e == 0)
+                    a[b + j + h] = d;
+                else if (e == 8)
+                    a[b + j + h] = mul_si(d, SIGN);
+                else
+                    a[b + j + h] = d * w32<SIGN>(e);
+            }
+        }
+    }
+    cplx t[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) t[k] = a[bitrev_c<N>(k)];
+#pragma unroll
+    for (int k = 0; k < N; ++k) a[k] = t[k];
+}
+
 // w_L^{SIGN m}, m < L, from the plan's table exp(-2 pi i m / L)
 template <int SIGN>
 __device__ __forceinline__ cplx twl(const cplx* __restrict__ tw, int m) {
@@ -412,10 +455,13 @@ struct RegE {
 
 // TS: stride into the twiddle table (1: tw has L entries; 3: tw is the table
 // of a length-3L transform, w_L^m = tw[3 m])
-template <int L, int SIGN, int TS = 1>
+template <int L, int SIGN, int TS = 1, bool IP = false>
 __device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
     constexpr int E = RegE<L>::E, T = L / E;
-    dft_reg<E, SIGN>(a);
+    if constexpr (IP)
+        dft_reg_ip<E, SIGN>(a);
+    else
+        dft_reg<E, SIGN>(a);
 #pragma unroll
     for (int k1 = 1; k1 < E; ++k1) a[k1] = a[k1] * twl<SIGN>(tw, ((t * k1) & (L - 1)) * TS);
 #pragma unroll
@@ -434,7 +480,7 @@ __device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t,
 }
 
 // inverse of the layout reg_fwd leaves (unnormalised, sign +1)
-template <int L, int TS = 1>
+template <int L, int TS = 1, bool IP = false>
 __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
     constexpr int E = RegE<L>::E, T = L / E;
     __syncthreads();   // buf reuse
@@ -452,12 +498,18 @@ __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t,
     __syncthreads();
 #pragma unroll
     for (int k1 = 0; k1 < E; ++k1) a[k1] = buf[k1 * (T + 1) + t];
-    dft_reg<E, +1>(a);
+    if constexpr (IP)
+        dft_reg_ip<E, +1>(a);
+    else
+        dft_reg<E, +1>(a);
 }
 
 #define RF_THREADS 128
-template <int L, bool ZC>
-__global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
+#ifndef RF_MINB512
+#define RF_MINB512 3
+#endif
+template <int L, bool ZC, bool IP = false>
+__global__ void __launch_bounds__(RF_THREADS, (L == 512 && IP) ? RF_MINB512 : 1) k_fft_reg(FftStage st) {
     constexpr int E = RegE<L>::E, T = L / E, CPB = RF_THREADS / T, CS = E * (T + 1) + 1;
     extern __shared__ cplx xs[];
     const int c = ZC ? threadIdx.x / T : threadIdx.x % CPB;
@@ -484,7 +536,7 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
     cplx* buf = xs + c * CS;
     cplx* out = st.out + (int64_t)blockIdx.y * st.out_s1 + (int64_t)col * st.out_s0;
     if (st.spec) {
-        reg_fwd<L, -1>(a, buf, t, st.tw);
+        reg_fwd<L, -1, 1, IP>(a, buf, t, st.tw);
         int64_t fcol = col;
         if (st.fold_y | st.fold_z) {
             int ky = col / st.spec_L2, kz = col - ky * st.spec_L2;
@@ -500,7 +552,7 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
                 for (int k2 = 0; k2 < T; ++k2)
                     a[s * T + k2] = a[s * T + k2] * sp[(int64_t)(t + T * s + E * k2) * st.spec_stride];
         }
-        reg_inv<L>(a, buf, t, st.tw);
+        reg_inv<L, 1, IP>(a, buf, t, st.tw);
 #pragma unroll
         for (int n1 = 0; n1 < E; ++n1) {
             const int i = t + T * n1;
@@ -509,9 +561,9 @@ __global__ void __launch_bounds__(RF_THREADS) k_fft_reg(FftStage st) {
         return;
     }
     if (st.sign < 0)
-        reg_fwd<L, -1>(a, buf, t, st.tw);
+        reg_fwd<L, -1, 1, IP>(a, buf, t, st.tw);
     else
-        reg_fwd<L, +1>(a, buf, t, st.tw);
+        reg_fwd<L, +1, 1, IP>(a, buf, t, st.tw);
 #pragma unroll
     for (int s = 0; s < E / T; ++s)
 #pragma unroll
@@ -527,12 +579,25 @@ static bool reg_launch(const FftStage& st, cudaStream_t s) {
     constexpr int E = RegE<L>::E, T = L / E, CPB = RF_THREADS / T, CS = E * (T + 1) + 1;
     const size_t smem = (size_t)CPB * CS * sizeof(cplx);
     static bool configured = false;
+    static const bool ip = [] {   // in-place E-point register DFTs (fewer live registers)
+        const char* e = getenv("FFTPIM_FFT_IP");
+        return e && e[0] == '1';
+    }();
     if (!configured) {
         cudaFuncSetAttribute(k_fft_reg<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_fft_reg<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_reg<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_reg<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     dim3 grid((st.nb0 + CPB - 1) / CPB, st.nb1);
+    if (ip) {
+        if (st.in_stride == 1)
+            k_fft_reg<L, true, true><<<grid, RF_THREADS, smem, s>>>(st);
+        else
+            k_fft_reg<L, false, true><<<grid, RF_THREADS, smem, s>>>(st);
+        return true;
+    }
     if (st.in_stride == 1)
         k_fft_reg<L, true><<<grid, RF_THREADS, smem, s>>>(st);
     else

@@ -1051,16 +1051,23 @@ void build(FftpimPlan* P) {
     }
     P->n_tiles = (npairs + CORR_TILE - 1) / CORR_TILE;
     P->info.pair_rows_source_order = 0;
-    if (!P->sweep && npairs > 0) {
+    if (npairs > 0) {
         // rows in source order for large pair lists (K4 gather locality, see
         // sort_pair_rows); FFTPIM_K4_SORT=0|1 overrides.  Exports then list each
-        // observer's pairs in source order (same set as the reference).
+        // observer's pairs in source order (same set as the reference).  Sweep
+        // plans permute their phase components with the rows.
         const char* e = getenv("FFTPIM_K4_SORT");
         if (e ? e[0] == '1' : npairs >= (int64_t)1 << 28) {
             size_t free_b = 0, tot_b = 0;
             CK(cudaMemGetInfo(&free_b, &tot_b));
             const size_t budget = (size_t)(0.6 * (double)free_b);
-            if (sort_pair_rows(P->pair_ptr, Mown, P->pair_src, P->pair_coef, P->pair_coef_r, P->pair_codeid, budget, s))
+            std::vector<cplx*> carr;
+            if (P->sweep)
+                for (int j = 0; j < P->sw_ncomp; ++j) carr.push_back(P->sw_comp + (int64_t)j * npairs);
+            else if (P->pair_coef)
+                carr.push_back(P->pair_coef);
+            if (sort_pair_rows(P->pair_ptr, Mown, P->pair_src, carr.data(), (int)carr.size(), P->pair_coef_r,
+                               P->pair_codeid, budget, s))
                 P->info.pair_rows_source_order = 1;
             else
                 cudaGetLastError();

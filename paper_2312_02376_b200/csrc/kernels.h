@@ -215,6 +215,6 @@ void launch_sweep_add_corr(cplx* u, const cplx* corr, const int* obs_perm, int64
 void build_corr_metadata(const int64_t* ptr, int64_t M, int64_t P, int64_t T, unsigned* bits, int64_t* seg_first,
                          int64_t* seg_base, int64_t* spans_tmp, int64_t* n_segments, cudaStream_t s);
 void launch_corr_tiles(const EvalArgs& a, cudaStream_t s);
-bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* coef, double* coef_r, unsigned char* codeid,
-                    size_t budget, cudaStream_t s);
+bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* const* carr, int ncarr, double* coef_r,
+                    unsigned char* codeid, size_t budget, cudaStream_t s);
 int64_t build_group_offsets(const int* src, int64_t P, int* base, unsigned short* off, cudaStream_t s);

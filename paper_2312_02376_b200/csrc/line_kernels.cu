@@ -925,6 +925,7 @@ struct FarWinArgs {
 
 template <int WF>
 __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, FarWinArgs f) {
+    constexpr int TPL = (WF * WF * WF + 31) / 32;
     constexpr int REC = 3 * WF + 2;
     extern __shared__ double fpw_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -966,48 +967,31 @@ __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, 
         f.win[6 * c + lane] = lo[lane];
         f.win[6 * c + 3 + lane] = ext[lane];
     }
-    // lanes = (slot, ia, ib): PPW points per warp step, each point's W_f x W_f
-    // (x, y) taps on its own lanes with the W_f z taps in registers.  Between
-    // flushes every accumulated point shares the open start (c0, c1, c2); a flush
-    // merges the slots in a fixed order (xor-free down shuffles) and slot 0 adds
-    // the run into the window.
-    constexpr int WW = WF * WF, PPW = 32 / WW;
-    const int slot = lane / WW, ab = lane % WW, ia = ab / WF, ib = ab % WF;
-    const bool lane_on = slot < PPW;
-    const bool tap_ok = lane_on && ia < fs.w[0] && ib < fs.w[1];
-    double accr[WF], acci[WF];
+    // this lane's taps (taps past a single-plane axis are skipped)
+    int ta[TPL], tb[TPL], tc[TPL];
+    bool tok[TPL];
 #pragma unroll
-    for (int ic = 0; ic < WF; ++ic) accr[ic] = acci[ic] = 0.0;
+    for (int t = 0; t < TPL; ++t) {
+        const int tp = lane + 32 * t;
+        tc[t] = tp % WF;
+        tb[t] = (tp / WF) % WF;
+        ta[t] = tp / (WF * WF);
+        tok[t] = tp < WF * WF * WF && ta[t] < fs.w[0] && tb[t] < fs.w[1] && tc[t] < fs.w[2];
+    }
+    double accr[TPL], acci[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) accr[t] = acci[t] = 0.0;
     int c0 = -1, c1 = 0, c2 = 0;
     auto flush = [&]() {
 #pragma unroll
-        for (int ic = 0; ic < WF; ++ic) {
-            double vr = accr[ic], vi = acci[ic];
-            double sr = vr, si = vi;
-#pragma unroll
-            for (int k = 1; k < PPW; ++k) {
-                sr += __shfl_down_sync(0xffffffffu, vr, k * WW);
-                si += __shfl_down_sync(0xffffffffu, vi, k * WW);
-            }
-            if (slot == 0 && tap_ok && ic < fs.w[2]) {
-                cplx& d = dst[((c0 - lo[0] + ia) * ext[1] + (c1 - lo[1] + ib)) * ext[2] + (c2 - lo[2] + ic)];
-                d.re += sr;
-                d.im += si;
-            }
-            accr[ic] = acci[ic] = 0.0;
+        for (int t = 0; t < TPL; ++t) {
+            if (!tok[t]) continue;
+            cplx& d = dst[((c0 - lo[0] + ta[t]) * ext[1] + (c1 - lo[1] + tb[t])) * ext[2] + (c2 - lo[2] + tc[t])];
+            d.re += accr[t];
+            d.im += acci[t];
+            accr[t] = acci[t] = 0.0;
         }
         __syncwarp();
-    };
-    auto add = [&](const double* r) {   // this lane's W_f taps of one point
-        const double qre = r[3 * WF], qim = r[3 * WF + 1];
-        const double wxy = r[ia] * r[WF + ib];
-        const double tr = qre * wxy, ti = qim * wxy;
-#pragma unroll
-        for (int ic = 0; ic < WF; ++ic) {
-            const double wz = r[2 * WF + ic];
-            accr[ic] = fma(tr, wz, accr[ic]);
-            acci[ic] = fma(ti, wz, acci[ic]);
-        }
     };
     __syncwarp();
     // pass 2: batches of 32 points, stencils computed by the loading lane
@@ -1026,31 +1010,21 @@ __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, 
         }
         __syncwarp();
         const int cnt = (int)min((int64_t)32, p1 - base);
-        for (int j0 = 0; j0 < cnt; j0 += PPW) {
-            // fast path: the whole step shares the open start
-            bool same = true;
+        for (int j = 0; j < cnt; ++j) {
+            const double* r = stage + j * REC;
+            const int s0 = sst[3 * j], s1 = sst[3 * j + 1], s2 = sst[3 * j + 2];
+            if (s0 != c0 || s1 != c1 || s2 != c2) {   // warp-uniform
+                if (c0 >= 0) flush();
+                c0 = s0;
+                c1 = s1;
+                c2 = s2;
+            }
+            const double qre = r[3 * WF], qim = r[3 * WF + 1];
 #pragma unroll
-            for (int k = 0; k < PPW; ++k) {
-                const int j = j0 + k;
-                if (j < cnt)
-                    same = same && sst[3 * j] == c0 && sst[3 * j + 1] == c1 && sst[3 * j + 2] == c2;
-            }
-            if (same) {
-                const int j = j0 + slot;
-                if (lane_on && j < cnt) add(stage + j * REC);
-                continue;
-            }
-            // slow path: the step's points one at a time
-            for (int k = 0; k < PPW && j0 + k < cnt; ++k) {
-                const int j = j0 + k;
-                const int s0 = sst[3 * j], s1 = sst[3 * j + 1], s2 = sst[3 * j + 2];
-                if (s0 != c0 || s1 != c1 || s2 != c2) {   // warp-uniform
-                    if (c0 >= 0) flush();
-                    c0 = s0;
-                    c1 = s1;
-                    c2 = s2;
-                }
-                if (slot == k) add(stage + j * REC);
+            for (int t = 0; t < TPL; ++t) {
+                const double wgt = (r[ta[t]] * r[WF + tb[t]]) * r[2 * WF + tc[t]];
+                accr[t] += wgt * qre;
+                acci[t] += wgt * qim;
             }
         }
     }

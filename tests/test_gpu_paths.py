@@ -58,9 +58,11 @@ def test_k1_ell_matches_computed_projection(case, tmp_path):
 @pytest.mark.parametrize("case", ["c1", "c2", "blobs3d", "tri", "g256"])
 def test_register_fft_matches_stockham_and_cufft(case, tmp_path):
     u_reg, _ = run_variant(case, {}, tmp_path, "reg")
-    if case == "g256":   # L = 512: the 8 x 8 x 8 kernel vs the E = 32 two-level one
+    if case == "g256":   # L = 512: the 8 x 8 x 8 kernel and in-place E = 32 DFTs vs the default
         u_e32, _ = run_variant(case, {"FFTPIM_FFT_R8": "1"}, tmp_path, "r8")
         assert rel_l2(u_reg, u_e32) <= 1e-13
+        u_ip, _ = run_variant(case, {"FFTPIM_FFT_IP": "1"}, tmp_path, "ip")
+        assert rel_l2(u_reg, u_ip) <= 1e-13
     u_smem, _ = run_variant(case, {"FFTPIM_FFT_REG": "0"}, tmp_path, "smem")
     if case == "tri":   # the radix-3 register kernels alone switched off
         u_r3, _ = run_variant(case, {"FFTPIM_FFT_REG3": "0"}, tmp_path, "noreg3")

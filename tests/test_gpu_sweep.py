@@ -104,6 +104,25 @@ def test_sweep_c5_subset(fp):
         del plan
 
 
+def test_sweep_source_ordered_rows(fp, monkeypatch):
+    """Sweep plans with rows in source order (the default for large pair lists;
+    the phase components are permuted with the rows): same potentials to 1e-13."""
+    name = "p2_dyn"
+    case = SMALL_CASES[name]
+    pos, q, obs = case_inputs(name)
+    shifts = [complex(case["kshift"][0]) + 0.07 * e for e in range(12)]
+    rng = np.random.default_rng(12)
+    Q = rng.normal(size=(len(shifts), q.size)) + 1j * rng.normal(size=(len(shifts), q.size))
+    cfg, box, src, ob, prm = objects(fp, case, pos, q, obs)
+    u0 = fp.build_sweep_plan(cfg, box, src, ob, prm, 0, shifts).evaluate(Q)
+    monkeypatch.setenv("FFTPIM_K4_SORT", "1")
+    sw = fp.build_sweep_plan(cfg, box, src, ob, prm, 0, shifts)
+    assert sw.info.pair_rows_source_order == 1
+    u1 = sw.evaluate(Q)
+    assert rel_l2(u1, u0) <= 1e-13
+    np.testing.assert_array_equal(sw.evaluate(Q), u1)
+
+
 def test_sweep_device_and_host_entries_agree(fp):
     """The device entry (caller stream, tensors) and the host entry (chunked
     uploads overlapping the chains) give bitwise identical potentials, and
