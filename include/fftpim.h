@@ -105,6 +105,8 @@ typedef struct FftpimInfo {
     int32_t pair_rows_source_order;   /* 1: each observer's pairs are stored (and exported) in source order,
                                          0: in the reference's discovery order (nearzone.py:374-478) */
     int32_t reserved2_;
+    int64_t k4_runs;            /* runs of consecutive sources in the run-encoded pair stream, padding
+                                   included (-1: K4 reads an int32 source index per pair) */
 } FftpimInfo;
 
 typedef struct FftpimPlan FftpimPlan;

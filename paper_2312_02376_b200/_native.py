@@ -50,6 +50,7 @@ class Info(C.Structure):
         ("graph_captures", C.c_int64), ("graph_instantiations", C.c_int64),
         ("k4_wide_groups", C.c_int64),
         ("pair_rows_source_order", C.c_int32), ("reserved2_", C.c_int32),
+        ("k4_runs", C.c_int64),
     ]
 
 

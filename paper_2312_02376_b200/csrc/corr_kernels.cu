@@ -604,9 +604,476 @@ bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* const* c
     return ok && cudaGetLastError() == cudaSuccess;
 }
 
+// ------------------------------------------------------------- K4, run-encoded sources
+// With rows in source order the source indices of consecutive pairs mostly
+// count up by one (the sorted sources of one z run of stencil cells), so the
+// int32 index per pair (4 of the 20 or 12 bytes a pair costs) is replaced by
+//   * one more bit per pair (run starts: tile starts, row starts, breaks in the
+//     index sequence) and
+//   * one int32 per run: bias = source of the run's first pair - its position e
+//     in the tile, so that src(e) = bias[rank(e)] + e, rank(e) = run starts at
+//     positions <= e, minus one (a popcount prefix over the tile's 8 run words).
+// Per tile the plan holds one 384-byte record: row-start words, run-start words,
+// first segment, run count, and the tile's first RUNS_BIAS_CAP biases (later
+// ones, rows in discovery order only, sit in an overflow array).
+// The kernel streams with bulk asynchronous copies (cp.async.bulk -> shared
+// memory, completion on an mbarrier) instead of per-thread loads: each warp owns
+// a ring of RUNS_STAGES stage buffers (a tile's coefficients + its record), lane
+// 0 issues the two copies of a tile RUNS_STAGES - 1 tiles ahead, and the
+// in-flight stream lives in shared memory, not registers.  Same pairs, same
+// order, same arithmetic as k_corr_tiles: bit-identical potentials.
+#ifndef RUNS_WARPS
+#define RUNS_WARPS 16
+#endif
+#ifndef RUNS_STAGES
+#define RUNS_STAGES 3
+#endif
+#define RUNS_BIAS_CAP 64
+#define RUNS_REC_WORDS 96   // 0-7 row-start words, 8-15 run-start words, 16-17 first segment,
+                            // 18-19 first overflow bias, 20 runs, 21-22 run-count prefix of the 8
+                            // groups (one byte each), 32-95 biases
+#define RUNS_QPAD CORR_TILE // zero charges past q_sorted[N): the last tile's padding pairs read them
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+// global -> shared bulk copy (bytes a multiple of 16, both addresses 16-byte
+// aligned), streamed through L2 with an evict-first policy
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+template <bool REAL>
+struct RunsStage {
+    static constexpr int coef_bytes = CORR_TILE * (REAL ? 8 : 16);
+    static constexpr int bytes = coef_bytes + RUNS_REC_WORDS * 4;
+};
+
+// lane 0: start the two copies of tile t into one stage (the coefficient
+// arrays are padded with zeros to whole tiles)
+template <bool REAL>
+__device__ __forceinline__ void runs_issue(const EvalArgs& a, int t, uint32_t stage, uint32_t bar, uint64_t pol) {
+    mbar_expect_tx(bar, RunsStage<REAL>::bytes);
+    if (REAL)
+        bulk_g2s(stage, a.coef_r + (int64_t)t * CORR_TILE, RunsStage<REAL>::coef_bytes, bar, pol);
+    else
+        bulk_g2s(stage, a.coef + (int64_t)t * CORR_TILE, RunsStage<REAL>::coef_bytes, bar, pol);
+    bulk_g2s(stage + RunsStage<REAL>::coef_bytes, a.run_rec + (int64_t)t * RUNS_REC_WORDS, RUNS_REC_WORDS * 4, bar, pol);
+}
+
+__device__ __forceinline__ int64_t meta_i64(unsigned m, int w) {
+    const unsigned lo = __shfl_sync(0xffffffffu, m, w), hi = __shfl_sync(0xffffffffu, m, w + 1);
+    return (int64_t)(((unsigned long long)hi << 32) | lo);
+}
+
+// Tile order of one warp.  Static: tiles warp, warp + stride, ... of a
+// persistent grid.  Dynamic (a.k4_counter): chunks of RUNS_CHUNK consecutive
+// tiles claimed from a global counter, one chunk ahead, so that launches sharing
+// the counter (the main grid beside the near chain, a helper grid after it)
+// and blocks that start late all drain one queue in stream order.
+#define RUNS_CHUNK 8
+struct TileQueue {
+    int cur, end, step, T;
+    unsigned next_raw;             // lane 0: the pre-claimed chunk
+    unsigned* counter;             // null: static
+    __device__ __forceinline__ void init(const EvalArgs& a, int T_, int warp, int warps, int lane) {
+        T = T_;
+        counter = reinterpret_cast<unsigned*>(a.k4_counter);
+        next_raw = 0;
+        if (counter) {
+            unsigned c = 0;
+            if (lane == 0) c = atomicAdd(counter, 1u);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            cur = (int)min((unsigned)T, c * RUNS_CHUNK);
+            end = min(cur + RUNS_CHUNK, T);
+            if (lane == 0 && cur < T) next_raw = atomicAdd(counter, 1u);
+            step = 1;
+        } else {
+            cur = blockIdx.x * warps + warp;
+            step = gridDim.x * warps;
+            end = T;
+        }
+    }
+    // the next tile of this warp (>= T: none left)
+    __device__ __forceinline__ int next(int lane) {
+        if (cur < end) {
+            const int t = cur;
+            cur += step;
+            return t;
+        }
+        if (!counter || cur >= T) return T;
+        const unsigned c = __shfl_sync(0xffffffffu, next_raw, 0);
+        cur = (int)min((unsigned)T, c * RUNS_CHUNK);
+        end = min(cur + RUNS_CHUNK, T);
+        if (cur >= T) return T;
+        if (lane == 0) next_raw = atomicAdd(counter, 1u);
+        return cur++;
+    }
+};
+
+// segmented accumulation of one tile in pair order with the row-start words in
+// registers (same operations and order as corr_reduce_tile)
+__device__ __forceinline__ void corr_reduce_tile_w(const EvalArgs& a, int lane, const double* cr, const double* ci,
+                                                   const double* qr, const double* qi, const unsigned* hw,
+                                                   int64_t sbase) {
+    double accr = 0.0, acci = 0.0;
+    int seg = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const double pr = cr[k] * qr[k] - ci[k] * qi[k];
+        const double pi = cr[k] * qi[k] + ci[k] * qr[k];
+        unsigned f = hw[k];
+        if (k == 0) f &= ~1u;   // a row starting at the tile start is segment 0 itself
+        if (f == 0u) {
+            accr += pr;
+            acci += pi;
+            continue;
+        }
+        int s = __ffs(f) - 1;
+        {
+            double vr = accr + (lane < s ? pr : 0.0), vi = acci + (lane < s ? pi : 0.0);
+            const cplx v = wsum(cplx{vr, vi});
+            if (lane == 0) a.seg_val[sbase + seg] = v;
+            ++seg;
+        }
+        f &= f - 1u;
+        while (f) {
+            const int s2 = __ffs(f) - 1;
+            const bool in = lane >= s && lane < s2;
+            const cplx v = wsum(cplx{in ? pr : 0.0, in ? pi : 0.0});
+            if (lane == 0) a.seg_val[sbase + seg] = v;
+            ++seg;
+            s = s2;
+            f &= f - 1u;
+        }
+        accr = lane >= s ? pr : 0.0;
+        acci = lane >= s ? pi : 0.0;
+    }
+    const cplx v = wsum(cplx{accr, acci});
+    if (lane == 0) a.seg_val[sbase + seg] = v;
+}
+
+template <bool REAL>
+__global__ void __launch_bounds__(32 * RUNS_WARPS, 1) k_corr_runs(EvalArgs a) {
+    extern __shared__ __align__(128) unsigned char runs_smem[];
+    constexpr int SS = RunsStage<REAL>::bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    const int T = (int)((a.n_pairs + CORR_TILE - 1) / CORR_TILE);
+    TileQueue tq;
+    tq.init(a, T, warp, warps, lane);
+    const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
+    unsigned char* my = runs_smem + (size_t)warp * RUNS_STAGES * SS;
+    const uint32_t stage0 = smem_addr(my);
+    const uint32_t bar0 = smem_addr(runs_smem + (size_t)warps * RUNS_STAGES * SS) + warp * RUNS_STAGES * 8;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < RUNS_STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // the warp reduces its tiles in the order the queue hands them out, so it only
+    // counts the tiles issued and not yet reduced
+    int pending = 0;
+#pragma unroll
+    for (int j = 0; j < RUNS_STAGES; ++j) {
+        const int tj = tq.next(lane);
+        if (tj < T) {
+            if (lane == 0) runs_issue<REAL>(a, tj, stage0 + j * SS, bar0 + 8 * j, pol);
+            ++pending;
+        }
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    const unsigned le_mask = 0xffffffffu >> (31 - lane);
+    while (pending > 0) {
+        mbar_wait(bar0 + 8 * s, ph);
+        const unsigned char* st = my + s * SS;
+        const uint4* rec4 = reinterpret_cast<const uint4*>(st + RunsStage<REAL>::coef_bytes);
+        const int* sbias_m1 = reinterpret_cast<const int*>(rec4 + 8) - 1;
+        const uint4 h0 = rec4[0], h1 = rec4[1], r0 = rec4[2], r1 = rec4[3], mt = rec4[4], mn = rec4[5];
+        const unsigned hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const unsigned rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const int64_t sbase = (int64_t)(((unsigned long long)mt.y << 32) | mt.x);
+        const int nruns = (int)mn.x;
+        // sources: rank of pair e among the run starts -> bias -> bias + e
+        int src[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const unsigned pk = k < 4 ? mn.y : mn.z;
+            src[k] = (int)((pk >> (8 * (k & 3))) & 0xffu) + __popc(rw[k] & le_mask);   // rank + 1
+        }
+        if (nruns <= RUNS_BIAS_CAP) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) src[k] = sbias_m1[src[k]] + (32 * k + lane);
+        } else {   // rows in discovery order: biases past the record
+            const int64_t ob = (int64_t)(((unsigned long long)mt.w << 32) | mt.z);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int r = src[k] - 1;
+                src[k] = (r < RUNS_BIAS_CAP ? sbias_m1[r + 1] : __ldg(a.run_bias + ob + (r - RUNS_BIAS_CAP))) +
+                         (32 * k + lane);
+            }
+        }
+        double qr[8], qi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (realq) {
+                qr[k] = a.q_re[src[k]];
+                qi[k] = 0.0;
+            } else {
+                const cplx qv = a.q_sorted[src[k]];
+                qr[k] = qv.re;
+                qi[k] = qv.im;
+            }
+        }
+        double cr[8], ci[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (REAL) {
+                cr[k] = reinterpret_cast<const double*>(st)[32 * k + lane];
+                ci[k] = 0.0;
+            } else {
+                const double2 c = reinterpret_cast<const double2*>(st)[32 * k + lane];
+                cr[k] = c.x;
+                ci[k] = c.y;
+            }
+        }
+        corr_reduce_tile_w(a, lane, cr, ci, qr, qi, hw, sbase);
+        // the stage is free again: refill it RUNS_STAGES tiles ahead
+        __syncwarp();
+        const int tn = tq.next(lane);
+        --pending;
+        if (tn < T) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                runs_issue<REAL>(a, tn, stage0 + s * SS, bar0 + 8 * s, pol);
+            }
+            ++pending;
+        }
+        if (++s == RUNS_STAGES) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
+size_t corr_runs_smem(bool real, int warps) {
+    return (size_t)warps * RUNS_STAGES * (real ? RunsStage<true>::bytes : RunsStage<false>::bytes) +
+           (size_t)warps * RUNS_STAGES * 8;
+}
+
+// ---- plan build of the run records
+// run-start bits over the pair positions padded to whole tiles: tile starts, row
+// starts, breaks in the source sequence, and the first padding position
+__global__ void k_run_words(const int* __restrict__ src, const unsigned* __restrict__ head, int64_t P, int64_t Ppad,
+                            unsigned* runw) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool f = false;
+    if (p < P) f = (p % CORR_TILE) == 0 || ((head[p >> 5] >> (p & 31)) & 1u) || src[p] != src[p - 1] + 1;
+    else if (p == P && p < Ppad) f = true;
+    const unsigned w = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && p < Ppad) runw[p >> 5] = w;
+}
+// runs past the record's RUNS_BIAS_CAP per tile
+__global__ void k_tile_overflow(const unsigned* __restrict__ runw, int64_t T, int64_t* ovf) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t > T) return;
+    int n = 0;
+    if (t < T)
+        for (int k = 0; k < 8; ++k) n += __popc(runw[t * 8 + k]);
+    ovf[t] = max(0, n - RUNS_BIAS_CAP);
+}
+// one warp per tile: the record and the overflow biases.  Padding pairs (zero
+// coefficients) read the zero charges q_sorted[N ..).
+__global__ void k_run_fill(const int* __restrict__ src, const unsigned* __restrict__ head,
+                           const unsigned* __restrict__ runw, const int64_t* __restrict__ seg_base,
+                           const int64_t* __restrict__ ovf_base, int64_t P, int64_t T, int64_t N, unsigned* recs,
+                           int* ovf, unsigned long long* total) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (t >= T) return;
+    const int64_t T0 = t * CORR_TILE;
+    const unsigned hw = lane < 8 ? head[(T0 >> 5) + lane] : 0u;
+    const unsigned rw = lane < 8 ? runw[(T0 >> 5) + lane] : 0u;
+    const unsigned long long ob = (unsigned long long)ovf_base[t], sb = (unsigned long long)seg_base[t];
+    const int c = __popc(rw);
+    int inc = c;   // inclusive prefix over lanes 0-7
+    for (int d = 1; d < 8; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+    }
+    const int n = __shfl_sync(0xffffffffu, inc, 7);
+    const unsigned ex = (unsigned)(inc - c);   // runs before group `lane`
+    unsigned pk0 = 0u, pk1 = 0u;
+    for (int k = 0; k < 4; ++k) {
+        pk0 |= (__shfl_sync(0xffffffffu, ex, k) & 0xffu) << (8 * k);
+        pk1 |= (__shfl_sync(0xffffffffu, ex, 4 + k) & 0xffu) << (8 * k);
+    }
+    const unsigned rws = __shfl_sync(0xffffffffu, rw, lane & 7);
+    unsigned* rec = recs + t * RUNS_REC_WORDS;
+    unsigned v = 0u;   // words 0-31: one per lane
+    if (lane < 8) v = hw;
+    else if (lane < 16) v = rws;
+    else if (lane == 16) v = (unsigned)(sb & 0xffffffffull);
+    else if (lane == 17) v = (unsigned)(sb >> 32);
+    else if (lane == 18) v = (unsigned)(ob & 0xffffffffull);
+    else if (lane == 19) v = (unsigned)(ob >> 32);
+    else if (lane == 20) v = (unsigned)n;
+    else if (lane == 21) v = pk0;
+    else if (lane == 22) v = pk1;
+    rec[lane] = v;
+    rec[32 + lane] = 0u;
+    rec[64 + lane] = 0u;
+    __syncwarp();
+    int pre = 0;
+    for (int k = 0; k < 8; ++k) {
+        const unsigned w = __shfl_sync(0xffffffffu, rw, k);
+        const int e = 32 * k + lane;
+        if ((w >> lane) & 1u) {
+            const int r = pre + __popc(w & ((1u << lane) - 1u));
+            const int b = (T0 + e < P ? src[T0 + e] : (int)N) - e;
+            if (r < RUNS_BIAS_CAP) rec[32 + r] = (unsigned)b;
+            else ovf[ob + (r - RUNS_BIAS_CAP)] = b;
+        }
+        pre += __popc(w);
+    }
+    if (lane == 0) atomicAdd(total, (unsigned long long)n);
+}
+
+// src <- bias[rank] + e (exports of plans that dropped their index array)
+__global__ void k_run_decode(const unsigned* __restrict__ recs, const int* __restrict__ ovf, int64_t P, int* src) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t T = (P + CORR_TILE - 1) / CORR_TILE;
+    if (t >= T) return;
+    const unsigned* rec = recs + t * RUNS_REC_WORDS;
+    const unsigned mw = rec[lane];
+    const int64_t ob = meta_i64(mw, 18);
+    const unsigned le_mask = 0xffffffffu >> (31 - lane);
+    int pre = -1;
+    for (int k = 0; k < 8; ++k) {
+        const unsigned rw = __shfl_sync(0xffffffffu, mw, 8 + k);
+        const int rank = pre + __popc(rw & le_mask);
+        pre += __popc(rw);
+        const int64_t p = t * CORR_TILE + 32 * k + lane;
+        if (p < P)
+            src[p] = (rank < RUNS_BIAS_CAP ? (int)rec[32 + rank] : ovf[ob + (rank - RUNS_BIAS_CAP)]) + 32 * k + lane;
+    }
+}
+
+// Builds the run records of a pair list whose metadata (head bits, tile segment
+// bases) exists.  *rec_out: (T, 96) words, *ovf_out: the overflow biases;
+// returns the number of runs, or -1 when the arrays do not fit.
+int64_t build_run_records(const int* src, const unsigned* head, const int64_t* seg_base, int64_t P, int64_t T,
+                          int64_t N, unsigned** rec_out, int** ovf_out, int64_t* bytes_out, cudaStream_t s) {
+    unsigned* runw = nullptr;
+    int64_t* cnt = nullptr;
+    int64_t* obase = nullptr;
+    unsigned long long* dtot = nullptr;
+    void* tmp = nullptr;
+    *rec_out = nullptr;
+    *ovf_out = nullptr;
+    const int64_t Ppad = T * CORR_TILE;
+    const int64_t W = Ppad / 32 + 8;
+    int64_t total = -1;
+    do {
+        if (cudaMalloc(&runw, sizeof(unsigned) * W) || cudaMalloc(&cnt, sizeof(int64_t) * (T + 1)) ||
+            cudaMalloc(&obase, sizeof(int64_t) * (T + 1)) || cudaMalloc(&dtot, sizeof(unsigned long long)))
+            break;
+        cudaMemsetAsync(runw, 0, sizeof(unsigned) * W, s);
+        cudaMemsetAsync(dtot, 0, sizeof(unsigned long long), s);
+        k_run_words<<<nblk64(Ppad, 256), 256, 0, s>>>(src, head, P, Ppad, runw);
+        k_tile_overflow<<<nblk64(T + 1, 256), 256, 0, s>>>(runw, T, cnt);
+        size_t bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, obase, (int)(T + 1), s);
+        if (cudaMalloc(&tmp, bytes + 16)) break;
+        cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, obase, (int)(T + 1), s);
+        int64_t h = 0;
+        cudaMemcpyAsync(&h, obase + T, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) break;
+        cudaFree(cnt);
+        cnt = nullptr;
+        cudaFree(tmp);
+        tmp = nullptr;
+        const size_t rec_bytes = sizeof(unsigned) * RUNS_REC_WORDS * (size_t)std::max<int64_t>(T, 1);
+        const size_t ovf_bytes = sizeof(int) * (size_t)(h + 4);
+        if (cudaMalloc(rec_out, rec_bytes) || cudaMalloc(ovf_out, ovf_bytes)) break;
+        k_run_fill<<<nblk64(T * 32, 256), 256, 0, s>>>(src, head, runw, seg_base, obase, P, T, N, *rec_out,
+                                                        *ovf_out, dtot);
+        unsigned long long ht = 0;
+        cudaMemcpyAsync(&ht, dtot, sizeof(ht), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) break;
+        fftpim_count_launch(4);
+        total = (int64_t)ht;
+        *bytes_out = (int64_t)(rec_bytes + ovf_bytes);
+    } while (0);
+    if (runw) cudaFree(runw);
+    if (cnt) cudaFree(cnt);
+    if (obase) cudaFree(obase);
+    if (dtot) cudaFree(dtot);
+    if (tmp) cudaFree(tmp);
+    if (total < 0) {
+        cudaGetLastError();
+        if (*rec_out) cudaFree(*rec_out);
+        if (*ovf_out) cudaFree(*ovf_out);
+        *rec_out = nullptr;
+        *ovf_out = nullptr;
+    }
+    return total;
+}
+
+void launch_run_decode(const unsigned* recs, const int* ovf, int64_t P, int* src, cudaStream_t s) {
+    const int64_t T = (P + CORR_TILE - 1) / CORR_TILE;
+    if (T > 0) k_run_decode<<<nblk64(T * 32, 256), 256, 0, s>>>(recs, ovf, P, src);
+    fftpim_count_launch();
+}
+
 void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.n_pairs == 0) return;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
+    if (a.run_rec) {
+        // whole chip: one 16-warp block per SM.  Capped (a.corr_blocks counts 8-warp
+        // blocks, the concurrent schedules): 8-warp blocks, so that other kernels
+        // fit beside a resident block.  a.k4_counter selects the shared tile queue.
+        const int warps = a.corr_blocks > 0 ? 8 : RUNS_WARPS;
+        int64_t cap = 148;
+        if (a.corr_blocks > 0) cap = a.corr_blocks;
+        if (a.corr_blocks < 0) cap = INT32_MAX;
+        const int blocks = (int)std::min<int64_t>((T + warps - 1) / warps, cap);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_corr_runs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)corr_runs_smem(true, RUNS_WARPS));
+            cudaFuncSetAttribute(k_corr_runs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)corr_runs_smem(false, RUNS_WARPS));
+            attr = true;
+        }
+        if (a.coef_r)
+            k_corr_runs<true><<<blocks, 32 * warps, corr_runs_smem(true, warps), s>>>(a);
+        else
+            k_corr_runs<false><<<blocks, 32 * warps, corr_runs_smem(false, warps), s>>>(a);
+        fftpim_count_launch();
+        return;
+    }
     // a.corr_blocks caps the grid (the concurrent schedule leaves SMs to the near chain)
     int64_t cap = 148 * CORR_MINB;
     if (a.corr_blocks > 0) cap = std::min<int64_t>(cap, a.corr_blocks);

@@ -402,6 +402,8 @@ void setup_fft_pipeline_shard(FftpimPlan* P, const int dims[3], cudaStream_t s) 
 }
 
 EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts);
+// run-encoded K4 stream by default?  (measured at C4: see DESIGN.md section 3)
+static bool k4_runs_default(const FftpimPlan* P) { return false && P->info.pair_rows_source_order == 1; }
 
 // Images of G_near for the shift ks (pgf.py:114-123): offsets i*L and phases
 // exp(-j i.(ks o L)), i in [-i_d, i_d]^dim.  axis >= 0 keeps only the images with
@@ -783,7 +785,8 @@ void build(FftpimPlan* P) {
         CK(cudaMemsetAsync(P->pad_in, 0, sizeof(cplx) * P->n_fft, s));   // padding stays zero: out-of-place forward FFT
     }
     }   // want_near
-    P->q_sorted = dalloc<cplx>(P, N);
+    P->q_sorted = dalloc<cplx>(P, N + CORR_QPAD);   // zero tail: padding pairs of k_corr_runs
+    CK(cudaMemset(P->q_sorted + N, 0, sizeof(cplx) * CORR_QPAD));
     {
         // tap-major K1 (3 active axes, orders 2..4) pays off for crowded cells
         // (clustered sources, C3: >= 1 point per stencil cell on average); sparse
@@ -1007,6 +1010,7 @@ void build(FftpimPlan* P) {
     }
     cplx* tables = dalloc<cplx>(P, tab_total);
     // fill pass
+    const int64_t npairs_pad = (npairs + CORR_TILE - 1) / CORR_TILE * CORR_TILE;
     P->pair_src = dalloc<int>(P, npairs);
     // image codes are only needed for operand export; skipped for huge pair counts (C3/C4)
     if (npairs <= (int64_t)1 << 31 || P->sweep) P->pair_codeid = dalloc<unsigned char>(P, npairs);
@@ -1037,13 +1041,18 @@ void build(FftpimPlan* P) {
     } else {
         launch_code_tables(tb, pg.ncodes, pg, im, tables, tab_total, s);
         if (P->npsp) {
-            P->pair_coef_r = dalloc<double>(P, npairs);
+            P->pair_coef_r = dalloc<double>(P, npairs_pad);   // zero tail: k_corr_runs copies whole tiles
+            CK(cudaMemsetAsync(P->pair_coef_r + npairs, 0, sizeof(double) * (npairs_pad - npairs), s));
             if (!P->sharded) {   // real-charge fast path of K4 (eval_kernels.cu k_permute_q)
-                P->q_re = dalloc<double>(P, N);
+                P->q_re = dalloc<double>(P, N + CORR_QPAD);
+                CK(cudaMemset(P->q_re + N, 0, sizeof(double) * CORR_QPAD));
                 P->q_flag = dalloc<int>(P, 1);
             }
         } else
-            P->pair_coef = dalloc<cplx>(P, npairs);
+        {
+            P->pair_coef = dalloc<cplx>(P, npairs_pad);
+            CK(cudaMemsetAsync(P->pair_coef + npairs, 0, sizeof(cplx) * (npairs_pad - npairs), s));
+        }
         P->info.real_coefficients = P->npsp ? 1 : 0;
         pa.coef = P->pair_coef;
         pa.coef_r = P->pair_coef_r;
@@ -1074,6 +1083,7 @@ void build(FftpimPlan* P) {
         }
     }
     P->info.k4_wide_groups = -1;
+    P->info.k4_runs = -1;
     if (!P->sweep && npairs > 0) {
         // 16-bit source offsets for K4 (2 B instead of 4 B per pair) when they fit
         // in memory; FFTPIM_K4_C16=0|1 overrides (default: large pair lists)
@@ -1101,6 +1111,34 @@ void build(FftpimPlan* P) {
                             &P->n_segments, s);
         dfree(P, spans);
         P->seg_val = dalloc<cplx>(P, P->n_segments);
+        // run-encoded sources + bulk-copy K4 (corr_kernels.cu k_corr_runs) for rows in
+        // source order; FFTPIM_K4_RUNS=0|1 overrides.  NPSP plans too large to export
+        // their pairs (> 2^31) drop the int32 index array afterwards.
+        const char* er = getenv("FFTPIM_K4_RUNS");
+        if (npairs > 0 && !P->pair_off16 && (er ? er[0] == '1' : k4_runs_default(P))) {
+            unsigned* meta = nullptr;
+            int* bias = nullptr;
+            int64_t rbytes = 0;
+            const int64_t nruns = build_run_records(P->pair_src, P->head_bits, P->seg_base, npairs, P->n_tiles, N,
+                                                    &meta, &bias, &rbytes, s);
+            if (nruns >= 0) {
+                P->run_rec = meta;
+                P->run_bias = bias;
+                P->allocations.push_back(meta);
+                P->allocations.push_back(bias);
+                P->device_bytes += rbytes;
+                P->info.k4_runs = nruns;
+                P->k4_counter = dalloc<unsigned long long>(P, 1);
+                // NPSP plans (no batched multi-RHS K4, which walks pair_src) are the
+                // ones that come close to the 180 GB: C3 frees 55 GB here
+                const char* ed = getenv("FFTPIM_K4_DROP_SRC");   // tests: exports decode the runs
+                if (ed ? ed[0] == '1' : npairs > (int64_t)1 << 31 && P->pair_coef_r) {
+                    P->device_bytes -= (int64_t)sizeof(int) * npairs;
+                    dfree(P, P->pair_src);
+                    P->pair_src = nullptr;
+                }
+            }
+        }
     }
     check_status(P, "correction coefficients");
     CK(cudaStreamSynchronize(s));
@@ -1352,6 +1390,8 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.pair_src = P->pair_src;
     a.pair_off16 = P->pair_off16;
     a.grp_base = P->grp_base;
+    a.run_rec = P->run_rec;
+    a.run_bias = P->run_bias;
     a.coef = P->pair_coef;
     a.coef_r = P->pair_coef_r;
     a.q_re = P->q_re;
@@ -1439,7 +1479,7 @@ static int batch_min() {
 }
 
 static bool batched_k4(const FftpimPlan* P, int64_t batch, int parts) {
-    return batch >= batch_min() && (parts & FFTPIM_NEAR) && P->pair_coef && !P->sweep && !P->sharded &&
+    return batch >= batch_min() && (parts & FFTPIM_NEAR) && P->pair_coef && P->pair_src && !P->sweep && !P->sharded &&
            P->N < ((int64_t)1 << 30) && P->info.n_pairs > 0;
 }
 
@@ -1523,6 +1563,63 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
         return;
     }
     const bool concurrent = P->info.n_pairs <= concurrent_max_pairs();
+    // Large plans with the run-encoded K4 (HBM-bound, little issue pressure): a
+    // main K4 grid of one 8-warp block per SM starts right after the permutation
+    // and streams beside the far chain, K1 and the FFT stages (on-chip-bound or
+    // short of bandwidth on their own), which run in the other half of every SM;
+    // when that chain is done a helper grid joins on the same tile queue
+    // (FFTPIM_K4_OVERLAP=0: chains in order).
+    static const int overlap_on = [] {
+        const char* e = getenv("FFTPIM_K4_OVERLAP");
+        return e ? atoi(e) : 1;
+    }();
+    if (!concurrent && overlap_on && P->run_rec && P->k4_counter && parts == FFTPIM_ALL) {
+        static const int main_blocks = [] {
+            const char* e = getenv("FFTPIM_K4A_BLOCKS");
+            return e ? atoi(e) : 148;
+        }();
+        static const int help_blocks = [] {
+            const char* e = getenv("FFTPIM_K4B_BLOCKS");
+            return e ? atoi(e) : 148;
+        }();
+        if (!P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
+        cudaStream_t sc = P->aux[1], sf = P->aux[2];
+        for (int64_t b = 0; b < batch; ++b) {
+            EvalArgs a = eval_args(P, q + 2 * b * P->N, u + 2 * b * P->M, parts);
+            launch_permute_q(a, s);
+            CK(cudaEventRecord(P->ev_fork, s));
+            EvalArgs ac = a;
+            ac.k4_counter = P->k4_counter;
+            ac.corr_blocks = main_blocks;
+            CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
+            CK(cudaMemsetAsync(P->k4_counter, 0, sizeof(unsigned long long), sc));
+            launch_corr_tiles(ac, sc);
+            CK(cudaEventRecord(P->ev_join[1], sc));
+            CK(cudaStreamWaitEvent(sf, P->ev_fork, 0));
+            launch_far_project(a, sf);
+            launch_far_sum(a, sf);
+            CK(cudaEventRecord(P->ev_join[2], sf));
+            launch_near_project(a, s);
+            if (P->custom_fft) {
+                for (int k = 0; k < 5; ++k)
+                    if (P->stage_on[k]) launch_fft_stage(P->stage[k], s);
+            } else {
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->pad_in, (cufftDoubleComplex*)P->work, CUFFT_FORWARD));
+                launch_spectrum_mul(a, s);
+                CKFFT(cufftExecZ2Z(P->fft_plan, (cufftDoubleComplex*)P->work, (cufftDoubleComplex*)P->work, CUFFT_INVERSE));
+                fftpim_count_launch(2);
+            }
+            CK(cudaStreamWaitEvent(s, P->ev_join[2], 0));
+            if (help_blocks > 0) {
+                ac.corr_blocks = help_blocks;
+                launch_corr_tiles(ac, s);
+            }
+            CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));
+            launch_observers(a, s);
+        }
+        CK(cudaGetLastError());
+        return;
+    }
     if (!concurrent) {
         if (parts & FFTPIM_NEAR && !P->custom_fft) CKFFT(cufftSetStream(P->fft_plan, s));
         for (int64_t b = 0; b < batch; ++b) {
@@ -2762,7 +2859,16 @@ int fftpim_plan_export(const FftpimPlan* cplan, int32_t which, void* dst, int64_
             }
         } else if (which == FFTPIM_PAIR_SRC) {
             need(npairs * 4);
-            CK(cudaMemcpy(psrc.data(), P->pair_src, sizeof(int) * npairs, cudaMemcpyDeviceToHost));
+            if (P->pair_src) {
+                CK(cudaMemcpy(psrc.data(), P->pair_src, sizeof(int) * npairs, cudaMemcpyDeviceToHost));
+            } else {   // run-encoded plan that dropped its index array
+                int* tmp = nullptr;
+                CK(cudaMalloc(&tmp, sizeof(int) * (size_t)std::max<int64_t>(npairs, 1)));
+                launch_run_decode(P->run_rec, P->run_bias, npairs, tmp, nullptr);
+                cudaError_t e = cudaMemcpy(psrc.data(), tmp, sizeof(int) * npairs, cudaMemcpyDeviceToHost);
+                cudaFree(tmp);
+                CK(e);
+            }
             CK(cudaMemcpy(sperm.data(), P->src_perm, sizeof(int) * N, cudaMemcpyDeviceToHost));
             int* o = (int*)dst;
             const int mask = P->sweep ? 0x3fffffff : -1;   // sweep plans pack the axis code in bits 30-31

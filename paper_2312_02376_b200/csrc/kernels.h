@@ -141,11 +141,14 @@ struct EvalArgs {
     int64_t n_pairs;
     const unsigned short* pair_off16;   // 16-bit source offsets per pair (non-null selects that K4)
     const int* grp_base;        // per 32-pair group: offset base, < 0 for int32 groups
+    const unsigned* run_rec;    // run-encoded sources (non-null selects k_corr_runs): 96 words per tile
+    const int* run_bias;        // biases past a tile record's 64 (source of a run's first pair - position)
     const unsigned* head_bits;  // bit p set where an observer's pair range starts
     const int64_t* seg_base;    // per CORR_TILE tile: global index of its first segment
     const int64_t* seg_first;   // per observer: global index of its first segment
     cplx* seg_val;              // (row, tile) segment sums
     int corr_blocks;            // K4 grid cap (0 = whole chip)
+    unsigned long long* k4_counter;   // k_corr_runs: shared tile queue (null: static tile order)
     // far
     StencilGeom fs, fo;
     const double* src_fw;
@@ -218,3 +221,7 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s);
 bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* const* carr, int ncarr, double* coef_r,
                     unsigned char* codeid, size_t budget, cudaStream_t s);
 int64_t build_group_offsets(const int* src, int64_t P, int* base, unsigned short* off, cudaStream_t s);
+int64_t build_run_records(const int* src, const unsigned* head, const int64_t* seg_base, int64_t P, int64_t T,
+                          int64_t N, unsigned** rec_out, int** ovf_out, int64_t* bytes_out, cudaStream_t s);
+#define CORR_QPAD 256   // zero charges kept past q_sorted[N) / q_re[N) (padding pairs of k_corr_runs)
+void launch_run_decode(const unsigned* recs, const int* ovf, int64_t P, int* src, cudaStream_t s);

@@ -161,6 +161,9 @@ struct FftpimPlan {
     int* pair_src = nullptr;      // (P) sorted source index
     unsigned short* pair_off16 = nullptr;   // (P) 16-bit offsets from the 32-pair group base (K4)
     int* grp_base = nullptr;      // (P/32 + 8) group bases, -1: the group reads pair_src
+    unsigned* run_rec = nullptr;  // (tiles, 96) run-encoded sources: tile records (corr_kernels.cu k_corr_runs)
+    int* run_bias = nullptr;      // overflow biases; pair_src may be dropped once these exist
+    unsigned long long* k4_counter = nullptr;   // tile queue shared by the overlapped K4 launches
     unsigned char* pair_codeid = nullptr;  // (P) code id (export only)
     cplx* pair_coef = nullptr;    // (P) complex coefficients (dynamic / static-shifted)
     double* pair_coef_r = nullptr;  // (P) real coefficients (NPSP)

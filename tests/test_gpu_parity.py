@@ -127,6 +127,43 @@ def test_source_ordered_pair_rows(fp, name, monkeypatch):
     np.testing.assert_array_equal(plan.evaluate(q), u)
 
 
+@pytest.mark.parametrize("name", list(SMALL_CASES))
+@pytest.mark.parametrize("sort", ["1", "0"])
+def test_run_encoded_pair_stream(fp, name, sort, monkeypatch):
+    """K4 with run-encoded sources and bulk-copy streaming (the default for
+    source-ordered rows): same pairs, order and arithmetic as the int32-index
+    kernel, so the potentials are bit-identical; with rows in discovery order
+    (sort = 0) tiles hold more than 64 runs and the global-memory bias path runs.
+    A plan that dropped its index array exports the same pairs (decoded runs)."""
+    case = SMALL_CASES[name]
+    pos, q, obs = case_inputs(name)
+    cfg, box, src, ob, prm = ref_objects(fp, case, pos, q, obs)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        monkeypatch.setenv("FFTPIM_K4_SORT", sort)
+        monkeypatch.setenv("FFTPIM_K4_RUNS", "0")
+        base = fp.build_plan(cfg, box, src, ob, prm)
+        monkeypatch.setenv("FFTPIM_K4_RUNS", "1")
+        monkeypatch.setenv("FFTPIM_K4_DROP_SRC", "1")
+        plan = fp.build_plan(cfg, box, src, ob, prm)
+    assert base.native.info.k4_runs == -1
+    n_pairs = plan.native.info.n_pairs
+    if n_pairs == 0:
+        assert plan.native.info.k4_runs == -1
+        return
+    assert 0 < plan.native.info.k4_runs <= n_pairs + 3 * ((n_pairs + 255) // 256)
+    u = plan.evaluate(q)
+    np.testing.assert_array_equal(u, base.evaluate(q))
+    np.testing.assert_array_equal(plan.evaluate(q), u)
+    np.testing.assert_array_equal(fp.eval_near(plan.near, q), fp.eval_near(base.near, q))
+    for a, b in ((plan.near.pair_obs, base.near.pair_obs), (plan.near.pair_src, base.near.pair_src),
+                 (plan.near.pair_coef, base.near.pair_coef)):
+        np.testing.assert_array_equal(a, b)
+    g = golden(f"small_{name}.npz")
+    assert rel_l2(u, g["u"]) <= TOL
+
+
 def _full(fp, c):
     from paper_2312_02376_b200.workloads import CONFIGS, make_inputs
     w = CONFIGS[c]
