@@ -623,10 +623,10 @@ bool sort_pair_rows(const int64_t* ptr, int64_t M, int* pair_src, cplx* const* c
 // in-flight stream lives in shared memory, not registers.  Same pairs, same
 // order, same arithmetic as k_corr_tiles: bit-identical potentials.
 #ifndef RUNS_WARPS
-#define RUNS_WARPS 16
+#define RUNS_WARPS 20
 #endif
 #ifndef RUNS_STAGES
-#define RUNS_STAGES 3
+#define RUNS_STAGES 2
 #endif
 #define RUNS_BIAS_CAP 64
 #define RUNS_REC_WORDS 96   // 0-7 row-start words, 8-15 run-start words, 16-17 first segment,
@@ -728,23 +728,21 @@ struct TileQueue {
     }
 };
 
-// segmented accumulation of one tile in pair order with the row-start words in
-// registers (same operations and order as corr_reduce_tile)
-__device__ __forceinline__ void corr_reduce_tile_w(const EvalArgs& a, int lane, const double* cr, const double* ci,
-                                                   const double* qr, const double* qi, const unsigned* hw,
-                                                   int64_t sbase) {
-    double accr = 0.0, acci = 0.0;
-    int seg = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const double pr = cr[k] * qr[k] - ci[k] * qi[k];
-        const double pi = cr[k] * qi[k] + ci[k] * qr[k];
-        unsigned f = hw[k];
-        if (k == 0) f &= ~1u;   // a row starting at the tile start is segment 0 itself
+// segmented accumulation in pair order, one 32-pair group at a time (same
+// operations and order as corr_reduce_tile)
+struct SegAcc {
+    double accr, acci;
+    int seg;
+    __device__ __forceinline__ void begin() {
+        accr = acci = 0.0;
+        seg = 0;
+    }
+    // f: row-start bits of the group (bit 0 of the tile's first group cleared by the caller)
+    __device__ __forceinline__ void add(const EvalArgs& a, int lane, double pr, double pi, unsigned f, int64_t sbase) {
         if (f == 0u) {
             accr += pr;
             acci += pi;
-            continue;
+            return;
         }
         int s = __ffs(f) - 1;
         {
@@ -766,8 +764,92 @@ __device__ __forceinline__ void corr_reduce_tile_w(const EvalArgs& a, int lane, 
         accr = lane >= s ? pr : 0.0;
         acci = lane >= s ? pi : 0.0;
     }
-    const cplx v = wsum(cplx{accr, acci});
-    if (lane == 0) a.seg_val[sbase + seg] = v;
+    __device__ __forceinline__ void end(const EvalArgs& a, int lane, int64_t sbase) {
+        const cplx v = wsum(cplx{accr, acci});
+        if (lane == 0) a.seg_val[sbase + seg] = v;
+    }
+};
+
+// one staged tile: sources from the record (rank of each pair among the run
+// starts -> bias -> bias + e), gathers, products, segmented sums
+template <bool REAL>
+__device__ __forceinline__ void runs_tile(const EvalArgs& a, const unsigned char* st, int lane, unsigned le_mask,
+                                          bool realq) {
+    const uint4* rec4 = reinterpret_cast<const uint4*>(st + RunsStage<REAL>::coef_bytes);
+    const int* sbias_m1 = reinterpret_cast<const int*>(rec4 + 8) - 1;
+    const uint4 h0 = rec4[0], h1 = rec4[1], r0 = rec4[2], r1 = rec4[3], mt = rec4[4], mn = rec4[5];
+    const unsigned hw[8] = {h0.x & ~1u, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+    const unsigned rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const int64_t sbase = (int64_t)(((unsigned long long)mt.y << 32) | mt.x);
+    const int nruns = (int)mn.x;
+    int src[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const unsigned pk = k < 4 ? mn.y : mn.z;
+        src[k] = (int)((pk >> (8 * (k & 3))) & 0xffu) + __popc(rw[k] & le_mask);   // rank + 1
+    }
+    if (nruns <= RUNS_BIAS_CAP) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) src[k] = sbias_m1[src[k]] + (32 * k + lane);
+    } else {   // rows in discovery order: biases past the record
+        const int64_t ob = (int64_t)(((unsigned long long)mt.w << 32) | mt.z);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int r = src[k] - 1;
+            src[k] = (r < RUNS_BIAS_CAP ? sbias_m1[r + 1] : __ldg(a.run_bias + ob + (r - RUNS_BIAS_CAP))) +
+                     (32 * k + lane);
+        }
+    }
+    double qr[8], qi[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (realq) {
+            qr[k] = a.q_re[src[k]];
+            qi[k] = 0.0;
+        } else {
+            const cplx qv = a.q_sorted[src[k]];
+            qr[k] = qv.re;
+            qi[k] = qv.im;
+        }
+    }
+    SegAcc acc;
+    acc.begin();
+    // most tiles lie inside one row (no row start past the tile's first pair):
+    // straight-line sums, the same operations in the same order
+    const bool one_row = ((hw[0] | hw[1] | hw[2] | hw[3]) | (hw[4] | hw[5] | hw[6] | hw[7])) == 0u;
+    if (one_row) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            double cr, ci;
+            if (REAL) {
+                cr = reinterpret_cast<const double*>(st)[32 * k + lane];
+                ci = 0.0;
+            } else {
+                const double2 c = reinterpret_cast<const double2*>(st)[32 * k + lane];
+                cr = c.x;
+                ci = c.y;
+            }
+            acc.accr += cr * qr[k] - ci * qi[k];
+            acc.acci += cr * qi[k] + ci * qr[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            double cr, ci;
+            if (REAL) {
+                cr = reinterpret_cast<const double*>(st)[32 * k + lane];
+                ci = 0.0;
+            } else {
+                const double2 c = reinterpret_cast<const double2*>(st)[32 * k + lane];
+                cr = c.x;
+                ci = c.y;
+            }
+            const double pr = cr * qr[k] - ci * qi[k];
+            const double pi = cr * qi[k] + ci * qr[k];
+            acc.add(a, lane, pr, pi, hw[k], sbase);
+        }
+    }
+    acc.end(a, lane, sbase);
 }
 
 template <bool REAL>
@@ -801,36 +883,100 @@ __global__ void __launch_bounds__(32 * RUNS_WARPS, 1) k_corr_runs(EvalArgs a) {
             ++pending;
         }
     }
-    int s = 0;
     uint32_t ph = 0;
     const unsigned le_mask = 0xffffffffu >> (31 - lane);
     while (pending > 0) {
-        mbar_wait(bar0 + 8 * s, ph);
-        const unsigned char* st = my + s * SS;
-        const uint4* rec4 = reinterpret_cast<const uint4*>(st + RunsStage<REAL>::coef_bytes);
-        const int* sbias_m1 = reinterpret_cast<const int*>(rec4 + 8) - 1;
-        const uint4 h0 = rec4[0], h1 = rec4[1], r0 = rec4[2], r1 = rec4[3], mt = rec4[4], mn = rec4[5];
-        const unsigned hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-        const unsigned rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        const int64_t sbase = (int64_t)(((unsigned long long)mt.y << 32) | mt.x);
-        const int nruns = (int)mn.x;
-        // sources: rank of pair e among the run starts -> bias -> bias + e
+#pragma unroll
+        for (int s = 0; s < RUNS_STAGES; ++s) {   // static stage addresses
+            if (pending == 0) break;
+            mbar_wait(bar0 + 8 * s, ph);
+            runs_tile<REAL>(a, my + s * SS, lane, le_mask, realq);
+            // the stage is free again: refill it RUNS_STAGES tiles ahead
+            __syncwarp();
+            const int tn = tq.next(lane);
+            --pending;
+            if (tn < T) {
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    runs_issue<REAL>(a, tn, stage0 + s * SS, bar0 + 8 * s, pol);
+                }
+                ++pending;
+            }
+        }
+        ph ^= 1u;
+    }
+}
+
+// ---- the same run-encoded stream through per-thread loads: the coefficients
+// and the tile record (3 coalesced words per lane: row/run words + rank prefixes,
+// biases 0-31, biases 32-63) are loaded one tile ahead into registers and the
+// biases are looked up with shuffles, so the whole L1 stays a cache for the q
+// gathers (the bulk-copy kernel above gives most of it to its stage buffers).
+template <bool REAL>
+struct RlTile {
+    double cr[8], ci[8];
+    unsigned w0, b0, b1;
+};
+
+template <bool REAL>
+__device__ __forceinline__ void rl_load(const EvalArgs& a, int t, int lane, RlTile<REAL>& d) {
+    const int64_t T0 = (int64_t)t * CORR_TILE;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (REAL) {
+            d.cr[k] = __ldcs(a.coef_r + T0 + 32 * k + lane);
+            d.ci[k] = 0.0;
+        } else {
+            const double2 c = __ldcs(reinterpret_cast<const double2*>(a.coef) + T0 + 32 * k + lane);
+            d.cr[k] = c.x;
+            d.ci[k] = c.y;
+        }
+    }
+    const unsigned* rec = a.run_rec + (int64_t)t * RUNS_REC_WORDS;
+    d.w0 = __ldcs(rec + lane);
+    d.b0 = __ldcs(rec + 32 + lane);
+    d.b1 = __ldcs(rec + 64 + lane);
+}
+
+template <bool REAL>
+__global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_rl(EvalArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = (int)((a.n_pairs + CORR_TILE - 1) / CORR_TILE);
+    TileQueue tq;
+    tq.init(a, T, warp, CORR_WARPS, lane);
+    const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
+    const unsigned le_mask = 0xffffffffu >> (31 - lane);
+    RlTile<REAL> cur, nxt;
+    int t = tq.next(lane);
+    if (t >= T) return;
+    rl_load<REAL>(a, t, lane, cur);
+    for (;;) {
+        const int tn = tq.next(lane);
+        if (tn < T) rl_load<REAL>(a, tn, lane, nxt);
+        const unsigned w0 = cur.w0;
+        const int64_t sbase = meta_i64(w0, 16);
+        const int nruns = (int)__shfl_sync(0xffffffffu, w0, 20);
+        const unsigned pk0 = __shfl_sync(0xffffffffu, w0, 21), pk1 = __shfl_sync(0xffffffffu, w0, 22);
         int src[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const unsigned pk = k < 4 ? mn.y : mn.z;
-            src[k] = (int)((pk >> (8 * (k & 3))) & 0xffu) + __popc(rw[k] & le_mask);   // rank + 1
+            const unsigned rw = __shfl_sync(0xffffffffu, w0, 8 + k);
+            const unsigned pk = k < 4 ? pk0 : pk1;
+            src[k] = (int)((pk >> (8 * (k & 3))) & 0xffu) + __popc(rw & le_mask) - 1;   // rank
         }
-        if (nruns <= RUNS_BIAS_CAP) {
+        if (nruns <= 32) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) src[k] = sbias_m1[src[k]] + (32 * k + lane);
-        } else {   // rows in discovery order: biases past the record
-            const int64_t ob = (int64_t)(((unsigned long long)mt.w << 32) | mt.z);
+            for (int k = 0; k < 8; ++k) src[k] = (int)__shfl_sync(0xffffffffu, cur.b0, src[k]) + (32 * k + lane);
+        } else {
+            const int64_t ob = meta_i64(w0, 18);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const int r = src[k] - 1;
-                src[k] = (r < RUNS_BIAS_CAP ? sbias_m1[r + 1] : __ldg(a.run_bias + ob + (r - RUNS_BIAS_CAP))) +
-                         (32 * k + lane);
+                const int r = src[k];
+                const int v0 = (int)__shfl_sync(0xffffffffu, cur.b0, r & 31);
+                const int v1 = (int)__shfl_sync(0xffffffffu, cur.b1, r & 31);
+                int b = r < 32 ? v0 : v1;
+                if (r >= RUNS_BIAS_CAP) b = __ldg(a.run_bias + ob + (r - RUNS_BIAS_CAP));
+                src[k] = b + (32 * k + lane);
             }
         }
         double qr[8], qi[8];
@@ -845,34 +991,91 @@ __global__ void __launch_bounds__(32 * RUNS_WARPS, 1) k_corr_runs(EvalArgs a) {
                 qi[k] = qv.im;
             }
         }
-        double cr[8], ci[8];
+        corr_reduce_tile(a, lane, cur.cr, cur.ci, qr, qi, w0, sbase);
+        if (tn >= T) break;
+        cur = nxt;
+    }
+}
+
+// ---- 16-bit source offsets on whole (zero-padded) tiles: the k_corr_tiles
+// pipeline with a 2-byte offset per pair instead of the 4-byte index, no tail
+// predicates, the 8 group bases of a tile riding in lanes 8-15 of the row-start
+// word register, and the (rare) wide groups re-read as int32 after the stream
+// loads, so the load phase has no branches.
+template <bool REAL>
+struct O16Tile {
+    int off[8];
+    double cr[8], ci[8];
+    unsigned word;   // lanes 0-7: row-start words, lanes 8-15: group bases
+    int64_t sbase;
+};
+
+template <bool REAL>
+__device__ __forceinline__ void o16_load(const EvalArgs& a, int t, int lane, O16Tile<REAL>& d) {
+    const int64_t T0 = (int64_t)t * CORR_TILE;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        d.off[k] = (int)__ldcs(a.pair_off16 + T0 + 32 * k + lane);
+        if (REAL) {
+            d.cr[k] = __ldcs(a.coef_r + T0 + 32 * k + lane);
+            d.ci[k] = 0.0;
+        } else {
+            const double2 c = __ldcs(reinterpret_cast<const double2*>(a.coef) + T0 + 32 * k + lane);
+            d.cr[k] = c.x;
+            d.ci[k] = c.y;
+        }
+    }
+    const int64_t g0 = (int64_t)t * (CORR_TILE / 32);
+    d.word = lane < 8 ? a.head_bits[g0 + lane] : (lane < 16 ? (unsigned)__ldcs(a.grp_base + g0 + lane - 8) : 0u);
+    d.sbase = a.seg_base[t];
+}
+
+template <bool REAL>
+__global__ void __launch_bounds__(32 * CORR_WARPS, CORR_MINB) k_corr_o16(EvalArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = (int)((a.n_pairs + CORR_TILE - 1) / CORR_TILE);
+    TileQueue tq;
+    tq.init(a, T, warp, CORR_WARPS, lane);
+    const bool realq = REAL && a.q_re && *(volatile const int*)a.q_flag == 0;
+    O16Tile<REAL> cur, nxt;
+    int t = tq.next(lane);
+    if (t >= T) return;
+    o16_load<REAL>(a, t, lane, cur);
+    for (;;) {
+        const int tn = tq.next(lane);
+        if (tn < T) o16_load<REAL>(a, tn, lane, nxt);
+        int src[8];
+        bool wide = false;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            if (REAL) {
-                cr[k] = reinterpret_cast<const double*>(st)[32 * k + lane];
-                ci[k] = 0.0;
+            const int gb = (int)__shfl_sync(0xffffffffu, cur.word, 8 + k);
+            src[k] = gb + cur.off[k];
+            wide |= gb < 0;
+        }
+        if (wide) {   // uniform: some group of this tile keeps int32 indices
+            const int64_t T0 = (int64_t)t * CORR_TILE;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int gb = (int)__shfl_sync(0xffffffffu, cur.word, 8 + k);
+                if (gb < 0) src[k] = T0 + 32 * k + lane < a.n_pairs ? a.pair_src[T0 + 32 * k + lane] : 0;
+            }
+        }
+        double qr[8], qi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (realq) {
+                qr[k] = a.q_re[src[k]];
+                qi[k] = 0.0;
             } else {
-                const double2 c = reinterpret_cast<const double2*>(st)[32 * k + lane];
-                cr[k] = c.x;
-                ci[k] = c.y;
+                const cplx qv = a.q_sorted[src[k]];
+                qr[k] = qv.re;
+                qi[k] = qv.im;
             }
         }
-        corr_reduce_tile_w(a, lane, cr, ci, qr, qi, hw, sbase);
-        // the stage is free again: refill it RUNS_STAGES tiles ahead
-        __syncwarp();
-        const int tn = tq.next(lane);
-        --pending;
-        if (tn < T) {
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                runs_issue<REAL>(a, tn, stage0 + s * SS, bar0 + 8 * s, pol);
-            }
-            ++pending;
-        }
-        if (++s == RUNS_STAGES) {
-            s = 0;
-            ph ^= 1u;
-        }
+        corr_reduce_tile(a, lane, cur.cr, cur.ci, qr, qi, cur.word, cur.sbase);
+        if (tn >= T) break;
+        cur = nxt;
+        t = tn;
     }
 }
 
@@ -1050,6 +1253,21 @@ void launch_run_decode(const unsigned* recs, const int* ovf, int64_t P, int* src
 void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.n_pairs == 0) return;
     const int64_t T = (a.n_pairs + CORR_TILE - 1) / CORR_TILE;
+    // FFTPIM_K4_RUNS_KERNEL=bulk|ldg (read per launch: launches are captured into graphs)
+    const char* erk = getenv("FFTPIM_K4_RUNS_KERNEL");
+    const int rl_kind = erk && erk[0] == 'l' ? 1 : 0;
+    if (a.run_rec && rl_kind == 1) {
+        int64_t cap = 148 * CORR_MINB;
+        if (a.corr_blocks > 0) cap = a.corr_blocks;
+        if (a.corr_blocks < 0) cap = INT32_MAX;
+        const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, cap);
+        if (a.coef_r)
+            k_corr_rl<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        else
+            k_corr_rl<false><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        fftpim_count_launch();
+        return;
+    }
     if (a.run_rec) {
         // whole chip: one 16-warp block per SM.  Capped (a.corr_blocks counts 8-warp
         // blocks, the concurrent schedules): 8-warp blocks, so that other kernels
@@ -1080,7 +1298,16 @@ void launch_corr_tiles(const EvalArgs& a, cudaStream_t s) {
     if (a.corr_blocks < 0) cap = INT32_MAX;   // one block per CORR_WARPS tiles (no grid-stride loop)
     const int blocks = (int)std::min<int64_t>((T + CORR_WARPS - 1) / CORR_WARPS, cap);
     if (a.pair_off16) {
-        if (a.coef_r)
+        static const int o16_kind = [] {   // FFTPIM_K4_C16_KERNEL=old: the three-stage k_corr_tiles_c16
+            const char* e = getenv("FFTPIM_K4_C16_KERNEL");
+            return e && e[0] == 'o' ? 0 : 1;
+        }();
+        if (o16_kind == 1) {
+            if (a.coef_r)
+                k_corr_o16<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+            else
+                k_corr_o16<false><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
+        } else if (a.coef_r)
             k_corr_tiles_c16<true><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);
         else
             k_corr_tiles_c16<false><<<blocks, 32 * CORR_WARPS, 0, s>>>(a);

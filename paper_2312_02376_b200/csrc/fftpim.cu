@@ -1097,7 +1097,8 @@ void build(FftpimPlan* P) {
             c16 = (double)npairs * 2.2 < 0.8 * (double)free_b;
         }
         if (c16) {
-            P->pair_off16 = dalloc<unsigned short>(P, npairs);
+            P->pair_off16 = dalloc<unsigned short>(P, npairs_pad);   // zero tail (whole tiles, k_corr_o16)
+            CK(cudaMemsetAsync(P->pair_off16 + npairs, 0, sizeof(unsigned short) * (npairs_pad - npairs), s));
             P->grp_base = dalloc<int>(P, (npairs + 31) / 32 + 8);
             P->info.k4_wide_groups = build_group_offsets(P->pair_src, npairs, P->grp_base, P->pair_off16, s);
         }
@@ -1328,8 +1329,8 @@ void build(FftpimPlan* P) {
         P->far_qg = dalloc<cplx>(P, nf);
         P->far_ug = dalloc<cplx>(P, nf);
     }
-    if (npairs <= concurrent_max_pairs() && getenv("FFTPIM_OBS_FUSED") == nullptr)
-        P->obs_pre = dalloc<cplx>(P, Mown);   // split observer pass (concurrent schedule)
+    if ((npairs <= concurrent_max_pairs() || P->run_rec) && getenv("FFTPIM_OBS_FUSED") == nullptr)
+        P->obs_pre = dalloc<cplx>(P, Mown);   // split observer pass (concurrent and overlap schedules)
     CK(cudaStreamSynchronize(s));
     dfree(P, d_cnt);
     dfree(P, d_src);
@@ -1578,6 +1579,10 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
             const char* e = getenv("FFTPIM_K4A_BLOCKS");
             return e ? atoi(e) : 148;
         }();
+        static const int obs_split = [] {
+            const char* e = getenv("FFTPIM_K4_OVERLAP_OBS");
+            return e ? atoi(e) : 1;
+        }();
         static const int help_blocks = [] {
             const char* e = getenv("FFTPIM_K4B_BLOCKS");
             return e ? atoi(e) : 148;
@@ -1610,12 +1615,28 @@ void evaluate_schedule(FftpimPlan* P, const double* q, double* u, int64_t batch,
                 fftpim_count_launch(2);
             }
             CK(cudaStreamWaitEvent(s, P->ev_join[2], 0));
+            // the interpolation (grid-tile pass, on-chip bound) also runs beside K4 when
+            // the plan has the sorted-order buffer; the finishing pass adds the row sums
+            const bool split = P->obs_pre && a.obs_pos && a.obs_cell_start && obs_split;
+            bool split_done = false;
+            if (split) {
+                EvalArgs ai = a;
+                ai.u_sorted = P->obs_pre;
+                ai.sw_e = -1;   // no K4 term
+                split_done = launch_observers_tile(ai, ai.obs_pos, ai.obs_cell_start, ai.obs_i0, s, 0);
+            }
             if (help_blocks > 0) {
                 ac.corr_blocks = help_blocks;
                 launch_corr_tiles(ac, s);
             }
             CK(cudaStreamWaitEvent(s, P->ev_join[1], 0));
-            launch_observers(a, s);
+            if (split_done) {
+                EvalArgs af = a;
+                af.u_sorted = P->obs_pre;
+                launch_finish_corr(af, s);
+            } else {
+                launch_observers(a, s);
+            }
         }
         CK(cudaGetLastError());
         return;

@@ -166,6 +166,7 @@ struct EvalArgs {
     int* far_win;
     int64_t far_n;
     cplx* obs_pre;              // far + K4 fix-up per sorted observer (split observer pass)
+    cplx* u_sorted;             // grid-tile observer pass: store near + far here in sorted order (no K4 term)
     const cplx* sw_corr;        // sweep: K4 sums (M, E) replace the segment fix-up
     int sw_E, sw_e;             // sw_e < 0: the observer pass leaves the K4 term out
     int parts;
@@ -190,6 +191,7 @@ int far_win_chunk(int64_t n);
 int64_t launch_max_tile_count(const StencilGeom& g, const int* ocs, cudaStream_t s);
 bool launch_observers_tile(const EvalArgs& a, const double* pos, const int* ocs, int64_t i0, cudaStream_t s,
                            int mode);
+void launch_finish_corr(const EvalArgs& a, cudaStream_t s);   // u = u_sorted + K4 row sums
 void launch_far_project(const EvalArgs& a, cudaStream_t s);
 size_t far_project_smem(int nf, int warps, int order);
 void launch_far_sum(const EvalArgs& a, cudaStream_t s);

@@ -838,8 +838,26 @@ __global__ void __launch_bounds__(K3T_NT, K3T_MINB) k_observers_tile(EvalArgs a,
                 }
             }
         }
-        a.u[a.obs_perm[i]] = cplx{ar, ai};
+        if (a.u_sorted)   // overlap schedule: K4 is still running, k_finish_corr adds its row sums
+            a.u_sorted[i] = cplx{ar, ai};
+        else
+            a.u[a.obs_perm[i]] = cplx{ar, ai};
     }
+}
+
+// u (caller order) = interpolated potentials (sorted order) + the K4 row sums
+__global__ void k_finish_corr(EvalArgs a) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.M) return;
+    const cplx c = corr_row_sum(a, i);
+    const cplx v = a.u_sorted[i];
+    a.u[a.obs_perm[i]] = cplx{v.re + c.re, v.im + c.im};
+}
+
+void launch_finish_corr(const EvalArgs& a, cudaStream_t s) {
+    if (a.M == 0) return;
+    k_finish_corr<<<(int)((a.M + 255) / 256), 256, 0, s>>>(a);
+    fftpim_count_launch();
 }
 
 template <int W, int WF, int MODE>

@@ -128,13 +128,15 @@ def test_source_ordered_pair_rows(fp, name, monkeypatch):
 
 
 @pytest.mark.parametrize("name", list(SMALL_CASES))
-@pytest.mark.parametrize("sort", ["1", "0"])
-def test_run_encoded_pair_stream(fp, name, sort, monkeypatch):
-    """K4 with run-encoded sources and bulk-copy streaming (the default for
-    source-ordered rows): same pairs, order and arithmetic as the int32-index
+@pytest.mark.parametrize("sort,kernel", [("1", "bulk"), ("0", "bulk"), ("1", "ldg"), ("0", "ldg")])
+def test_run_encoded_pair_stream(fp, name, sort, kernel, monkeypatch):
+    """K4 with run-encoded sources (opt-in, FFTPIM_K4_RUNS=1), streamed with bulk
+    asynchronous copies into shared memory (cp.async.bulk + mbarrier) or with
+    per-thread loads: same pairs, order and arithmetic as the int32-index
     kernel, so the potentials are bit-identical; with rows in discovery order
-    (sort = 0) tiles hold more than 64 runs and the global-memory bias path runs.
+    (sort = 0) tiles hold more than 64 runs and the overflow-bias path runs.
     A plan that dropped its index array exports the same pairs (decoded runs)."""
+    monkeypatch.setenv("FFTPIM_K4_RUNS_KERNEL", kernel)
     case = SMALL_CASES[name]
     pos, q, obs = case_inputs(name)
     cfg, box, src, ob, prm = ref_objects(fp, case, pos, q, obs)
