@@ -1519,7 +1519,7 @@ static void evaluate_batched(FftpimPlan* P, const double* q, double* u, int64_t 
         CK(cudaStreamWaitEvent(sc, P->ev_fork, 0));
         launch_batch_permute((const cplx*)qb, P->src_perm, P->N, E, P->bt_qt, sc);
         launch_corr_sweep(P->pair_ptr, P->pair_src, P->pair_coef, 1, P->info.n_pairs, P->bt_qt, P->N, E, P->bt_omega,
-                          P->bt_corr, P->M, sc);
+                          P->bt_corr, P->M, sc, P->info.pair_rows_source_order == 1);
         for (int e = 0; e < E; ++e) {
             EvalArgs a = eval_args(P, qb + 2 * (int64_t)e * P->N, ub + 2 * (int64_t)e * P->M, parts);
             a.sw_e = -1;   // the K4 term is added below
@@ -2241,7 +2241,7 @@ static void sweep_k4(FftpimPlan* P, const double* q, cudaStream_t s) {
     const int E = P->sw_E, NS = P->sw_ncomp + 2;
     launch_sweep_permute((const cplx*)q, P->src_perm, P->N, E, P->sw_omega, NS, P->prob.i_d, P->sw_qt, s);
     launch_corr_sweep(P->pair_ptr, P->pair_src, P->sw_comp, P->sw_ncomp, P->info.n_pairs, P->sw_qt, P->N, E,
-                      P->sw_omega, P->sw_corr, P->M, s);
+                      P->sw_omega, P->sw_corr, P->M, s, P->info.pair_rows_source_order == 1);
 }
 
 // `ready` (host entry): event e marks excitation e's charges resident; chain e

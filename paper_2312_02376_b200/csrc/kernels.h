@@ -211,7 +211,8 @@ void launch_sweep_pack_src(int* pair_src, const unsigned char* codeid, const sig
 void launch_sweep_permute(const cplx* q, const int* perm, int64_t N, int E, const cplx* omega, int NS, int h,
                           cplx* qt3, cudaStream_t s);
 void launch_corr_sweep(const int64_t* ptr, const int* pair_src, const cplx* comp, int ncomp, int64_t P,
-                       const cplx* qt3, int64_t N, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s);
+                       const cplx* qt3, int64_t N, int E, const cplx* omega, cplx* corr, int64_t M, cudaStream_t s,
+                       bool sorted_rows);
 void launch_batch_permute(const cplx* q, const int* perm, int64_t N, int E, cplx* qt, cudaStream_t s);
 void launch_sweep_add_corr(cplx* u, const cplx* corr, const int* obs_perm, int64_t M, int E, cudaStream_t s);
 
