@@ -505,6 +505,9 @@ __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t,
 }
 
 #define RF_THREADS 128
+#ifndef FFT_PF_FOLDED   // L2 prefetch of the spectrum rows also when the table is read at folded columns
+#define FFT_PF_FOLDED 0   // measured slower at C4 (x stage 1.41 -> 1.64 ms)
+#endif
 #ifndef RF_MINB512
 #define RF_MINB512 3
 #endif
@@ -516,11 +519,30 @@ __global__ void __launch_bounds__(RF_THREADS, (L == 512 && IP) ? RF_MINB512 : 1)
     const int t = ZC ? threadIdx.x % T : threadIdx.x / CPB;
     const int col = blockIdx.x * CPB + c;
     const bool okc = col < st.nb0;
-    if (st.spec && st.spec_s0 == 1 && !(st.fold_y | st.fold_z)) {
+    bool pf = st.spec && st.spec_s0 == 1;
+    int64_t pf_col = (int64_t)blockIdx.x * CPB;
+    const int pf_n = min(CPB, st.nb0 - (int)blockIdx.x * CPB);
+    if (pf && (st.fold_y | st.fold_z)) {
+        // folded table: the block's columns map to a contiguous (possibly reversed)
+        // run of folded columns when they stay inside one ky row and on one side of the fold
+        auto fold = [&](int cc) {
+            int ky = cc / st.spec_L2, kz = cc - ky * st.spec_L2;
+            if (st.fold_y && 2 * ky > st.fold_y) ky = st.fold_y - ky;
+            if (st.fold_z && 2 * kz > st.fold_z) kz = st.fold_z - kz;
+            return (int64_t)ky * st.spec_L2 + kz;
+        };
+        const int c0 = (int)blockIdx.x * CPB;
+        const int64_t f0 = fold(c0), f1 = fold(c0 + pf_n - 1);
+        pf = (f1 - f0 == pf_n - 1) || (f0 - f1 == pf_n - 1);
+        pf_col = f0 < f1 ? f0 : f1;
+        static_assert(FFT_PF_FOLDED == 0 || FFT_PF_FOLDED == 1, "");
+        if (!FFT_PF_FOLDED) pf = false;
+    }
+    if (pf) {
         // pull this block's spectrum rows (CPB consecutive columns per k) into L2
         // now; they are read after the forward transform
-        const int ncols = min(CPB, st.nb0 - (int)blockIdx.x * CPB);
-        const cplx* sp0 = st.spec + (int64_t)blockIdx.y * st.spec_s1 + (int64_t)blockIdx.x * CPB;
+        const int ncols = pf_n;
+        const cplx* sp0 = st.spec + (int64_t)blockIdx.y * st.spec_s1 + pf_col;
         for (int k = threadIdx.x; k < L; k += RF_THREADS)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sp0 + (int64_t)k * st.spec_stride),
                          "r"(ncols * (int)sizeof(cplx))
