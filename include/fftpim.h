@@ -196,7 +196,17 @@ enum FftpimOperand {
     FFTPIM_PAIR_CODE = 3,       /* int8  (P,3)          NearZonePlan.pair_code */
     FFTPIM_PAIR_COEF = 4,       /* complex128 (P)       NearZonePlan.pair_coef */
     FFTPIM_FAR_KERNEL = 5,      /* complex128 (2n-1)^3  FarZonePlan.kernel     */
-    FFTPIM_KERNEL_HAT = 6       /* complex128 fft_dims  NearZonePlan.kernel_hat (numpy scaling) */
+    FFTPIM_KERNEL_HAT = 6,      /* complex128 fft_dims  NearZonePlan.kernel_hat (numpy scaling) */
+    /* Lagrange stencils (grids.py:110-140) in the caller's point order: starts int32 (n, 3),
+     * weights float64 (n, 3, order + 1) (single-plane axes: weight 1 then zeros) */
+    FFTPIM_NEAR_SRC_START = 7,  /* NearZonePlan.proj_op.axis_starts    */
+    FFTPIM_NEAR_SRC_W = 8,      /* NearZonePlan.proj_op.axis_weights   */
+    FFTPIM_NEAR_OBS_START = 9,  /* NearZonePlan.interp_op.axis_starts  */
+    FFTPIM_NEAR_OBS_W = 10,     /* NearZonePlan.interp_op.axis_weights */
+    FFTPIM_FAR_SRC_START = 11,  /* FarZonePlan.proj_op.axis_starts     */
+    FFTPIM_FAR_SRC_W = 12,      /* FarZonePlan.proj_op.axis_weights    */
+    FFTPIM_FAR_OBS_START = 13,  /* FarZonePlan.interp_op.axis_starts   */
+    FFTPIM_FAR_OBS_W = 14       /* FarZonePlan.interp_op.axis_weights  */
 };
 FFTPIM_API int fftpim_plan_export(const FftpimPlan* plan, int32_t which, void* dst, int64_t bytes);
 

@@ -18,6 +18,8 @@ LIB_PATH = os.environ.get("FFTPIM_LIB") or os.path.join(os.path.dirname(os.path.
 OK, VALIDATION, DOMAIN, WOOD, NOT_CONVERGED, SEPARATION, KERNEL_CACHE, CUDA, VALUE = range(9)
 NEAR, FAR, ALL = 1, 2, 3
 PAIR_OBS, PAIR_SRC, PAIR_CODE, PAIR_COEF, FAR_KERNEL, KERNEL_HAT = 1, 2, 3, 4, 5, 6
+(NEAR_SRC_START, NEAR_SRC_W, NEAR_OBS_START, NEAR_OBS_W,
+ FAR_SRC_START, FAR_SRC_W, FAR_OBS_START, FAR_OBS_W) = range(7, 15)
 
 
 class Problem(C.Structure):

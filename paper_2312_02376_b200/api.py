@@ -180,6 +180,11 @@ class NativePlan:
             out = np.empty(tuple(2 * d - 1 if d > 1 else 1 for d in self.info.far_dims), dtype=np.complex128)
         elif which == nat.KERNEL_HAT:
             out = np.empty(tuple(self.info.fft_dims), dtype=np.complex128)
+        elif nat.NEAR_SRC_START <= which <= nat.FAR_OBS_W:
+            k = which - nat.NEAR_SRC_START
+            n = self.n_observers if k & 2 else self.n_sources
+            width = (self.params.far_order if k >= 4 else self.params.near_order) + 1
+            out = np.empty((n, 3, width), dtype=np.float64) if k & 1 else np.empty((n, 3), dtype=np.int32)
         else:
             raise ValueError(f"unknown operand {which}")
         nat.check(self._lib.fftpim_plan_export(self._h, which, out.ctypes.data, out.nbytes))
@@ -219,6 +224,52 @@ class _LazyPairs:
         return self._arr
 
 
+@dataclass(frozen=True)
+class SparseInterpOperator:
+    """Stencil data of one point set on one grid (grids.py:143-165 field names), read
+    back from the device plan.  A view for inspection and parity checks: projection
+    and interpolation themselves run inside `plan.evaluate` on the GPU."""
+    grid: UniformGrid
+    order: int
+    role: str                          # "project" or "interpolate"
+    axis_starts: np.ndarray            # (P, 3) int64
+    axis_weights: tuple                # (P, q_a + 1) each; (P, 1) ones on single-plane axes
+
+    @property
+    def n_points(self) -> int:
+        return self.axis_starts.shape[0]
+
+    @property
+    def stencil_size(self) -> int:
+        return int(np.prod([w.shape[1] for w in self.axis_weights]))
+
+    def _offsets(self):
+        return [self.axis_starts[:, a][:, None] + np.arange(self.axis_weights[a].shape[1])[None, :]
+                for a in range(3)]
+
+    @property
+    def flat_index(self) -> np.ndarray:
+        """(P, S) C-order node indices of every stencil tap (grids.py:200-206)."""
+        ox, oy, oz = self._offsets()
+        _, gy, gz = self.grid.dims
+        flat = ox[:, :, None, None] * (gy * gz) + oy[:, None, :, None] * gz + oz[:, None, None, :]
+        return flat.astype(np.int32).reshape(self.n_points, -1)
+
+    @property
+    def flat_weight(self) -> np.ndarray:
+        """(P, S) tensor-product weights (grids.py:207-210)."""
+        wx, wy, wz = self.axis_weights
+        w3 = wx[:, :, None, None] * wy[:, None, :, None] * wz[:, None, None, :]
+        return w3.reshape(self.n_points, -1)
+
+
+def _operator_view(native, grid, order, role, which_start, which_w) -> SparseInterpOperator:
+    starts = native.export(which_start).astype(np.int64)
+    w = native.export(which_w)
+    weights = tuple(np.ascontiguousarray(w[:, a, :1] if grid.dims[a] == 1 else w[:, a, :]) for a in range(3))
+    return SparseInterpOperator(grid, order, role, starts, weights)
+
+
 class NearZonePlan:
     """Near-zone view of a native plan (nearzone.py:55-124 field names)."""
 
@@ -240,6 +291,7 @@ class NearZonePlan:
         self.coincident_kernel_terms = int(info.coincident_kernel_terms)
         self._lazy = {k: _LazyPairs(native, k) for k in (nat.PAIR_OBS, nat.PAIR_SRC, nat.PAIR_CODE,
                                                           nat.PAIR_COEF, nat.KERNEL_HAT)}
+        self._ops = {}
 
     n_sources = property(lambda self: self.native.n_sources)
     n_observers = property(lambda self: self.native.n_observers)
@@ -248,6 +300,60 @@ class NearZonePlan:
     pair_code = property(lambda self: self._lazy[nat.PAIR_CODE].get())
     pair_coef = property(lambda self: self._lazy[nat.PAIR_COEF].get())
     kernel_hat = property(lambda self: self._lazy[nat.KERNEL_HAT].get())
+
+    @property
+    def d_er(self) -> float:
+        """Error-correction range (nearzone.py:204)."""
+        active = [a for a in range(3) if self.grid.dims[a] > 1]
+        return self.er_range_boxes * max(self.grid.spacing[a] for a in active)
+
+    @property
+    def proj_op(self) -> SparseInterpOperator:
+        if "proj" not in self._ops:
+            self._ops["proj"] = _operator_view(self.native, self.grid, self.order, "project",
+                                               nat.NEAR_SRC_START, nat.NEAR_SRC_W)
+        return self._ops["proj"]
+
+    @property
+    def interp_op(self) -> SparseInterpOperator:
+        if "interp" not in self._ops:
+            self._ops["interp"] = _operator_view(self.native, self.grid, self.order, "interpolate",
+                                                 nat.NEAR_OBS_START, nat.NEAR_OBS_W)
+        return self._ops["interp"]
+
+    @property
+    def seg_obs(self) -> np.ndarray:
+        """Observers owning at least one pair (nearzone.py:470-476)."""
+        cnt = np.bincount(self.pair_obs, minlength=self.n_observers)
+        return np.nonzero(cnt)[0]
+
+    @property
+    def seg_starts(self) -> np.ndarray:
+        """reduceat segment starts into the pair arrays (nearzone.py:470-476)."""
+        cnt = np.bincount(self.pair_obs, minlength=self.n_observers)
+        ends = np.cumsum(cnt)
+        return (ends - cnt)[np.nonzero(cnt)[0]]
+
+    @property
+    def kernel_disp(self) -> np.ndarray:
+        """Raw displacement table (2Nx-1, 2Ny-1, 2Nz-1) (nearzone.py:212-227), recovered from
+        the device's kernel_hat by undoing the circulant embedding (nearzone.py:127-147)."""
+        dims = self.grid.dims
+        c = np.fft.ifftn(self.kernel_hat)
+        out = np.zeros(tuple(2 * d - 1 if d > 1 else 1 for d in dims), dtype=complex)
+        import itertools
+        for neg in itertools.product(*[(0, 1) if d > 1 else (0,) for d in dims]):
+            sl_c, sl_k = [], []
+            for axis, ng in enumerate(neg):
+                n = dims[axis]
+                if n == 1:
+                    sl_c.append(slice(0, 1)); sl_k.append(slice(0, 1))
+                elif not ng:
+                    sl_c.append(slice(0, n)); sl_k.append(slice(n - 1, 2 * n - 1))
+                else:
+                    sl_c.append(slice(n + 1, 2 * n)); sl_k.append(slice(0, n - 1))
+            out[tuple(sl_k)] = c[tuple(sl_c)]
+        return out
 
 
 class FarZonePlan:
@@ -267,6 +373,7 @@ class FarZonePlan:
         self.observer_grid = UniformGrid(dims, tuple(v / 2.0 for v in h), h)
         self.kernel_terms = int(info.kernel_terms)
         self._kernel = None
+        self._ops = {}
 
     n_sources = property(lambda self: self.native.n_sources)
     n_observers = property(lambda self: self.native.n_observers)
@@ -276,6 +383,20 @@ class FarZonePlan:
         if self._kernel is None:
             self._kernel = self.native.export(nat.FAR_KERNEL)
         return self._kernel
+
+    @property
+    def proj_op(self) -> SparseInterpOperator:
+        if "proj" not in self._ops:
+            self._ops["proj"] = _operator_view(self.native, self.source_grid, self.order, "project",
+                                               nat.FAR_SRC_START, nat.FAR_SRC_W)
+        return self._ops["proj"]
+
+    @property
+    def interp_op(self) -> SparseInterpOperator:
+        if "interp" not in self._ops:
+            self._ops["interp"] = _operator_view(self.native, self.observer_grid, self.order, "interpolate",
+                                                 nat.FAR_OBS_START, nat.FAR_OBS_W)
+        return self._ops["interp"]
 
 
 @dataclass(frozen=True)

@@ -2856,6 +2856,35 @@ int fftpim_plan_export(const FftpimPlan* cplan, int32_t which, void* dst, int64_
             for (int64_t i = 0; i < 2 * P->n_fft; ++i) d[i] *= (double)P->n_fft;
             return FFTPIM_OK;
         }
+        if (which >= FFTPIM_NEAR_SRC_START && which <= FFTPIM_FAR_OBS_W) {
+            // stencils are held in sorted order; rows go back to the caller's order
+            const bool far = which >= FFTPIM_FAR_SRC_START, obs = ((which - FFTPIM_NEAR_SRC_START) & 2) != 0;
+            const bool wts = ((which - FFTPIM_NEAR_SRC_START) & 1) != 0;
+            const int64_t n = obs ? M : N;
+            const int Wd = (far ? P->prob.far_order : P->prob.near_order) + 1;
+            const double* dw = far ? (obs ? P->obs_fw : P->src_fw) : (obs ? P->obs_w : P->src_w);
+            const int* ds = far ? (obs ? P->obs_fstart : P->src_fstart) : (obs ? P->obs_start : P->src_start);
+            if (!dw || !ds) throw Fail{FFTPIM_VALUE, "this plan does not hold the requested stencils"};
+            if (P->sharded && obs) throw Fail{FFTPIM_VALUE, "observer stencils of a slab shard cover its own range only"};
+            std::vector<int> perm(n);
+            CK(cudaMemcpy(perm.data(), obs ? P->obs_perm : P->src_perm, sizeof(int) * n, cudaMemcpyDeviceToHost));
+            if (wts) {
+                need(n * 3 * Wd * 8);
+                std::vector<double> h((size_t)n * 3 * Wd);
+                CK(cudaMemcpy(h.data(), dw, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+                double* o = (double*)dst;
+                for (int64_t i = 0; i < n; ++i)
+                    std::copy(h.begin() + i * 3 * Wd, h.begin() + (i + 1) * 3 * Wd, o + (int64_t)perm[i] * 3 * Wd);
+            } else {
+                need(n * 3 * 4);
+                std::vector<int> h((size_t)n * 3);
+                CK(cudaMemcpy(h.data(), ds, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
+                int* o = (int*)dst;
+                for (int64_t i = 0; i < n; ++i)
+                    for (int a = 0; a < 3; ++a) o[(int64_t)perm[i] * 3 + a] = h[i * 3 + a];
+            }
+            return FFTPIM_OK;
+        }
         if (which < FFTPIM_PAIR_OBS || which > FFTPIM_PAIR_COEF) throw Fail{FFTPIM_VALUE, "unknown operand"};
         std::vector<int64_t> ptr(M + 1);
         std::vector<int> operm(M), sperm(N), psrc(npairs);

@@ -129,3 +129,39 @@ def test_retained_outputs_update_one_graph(fp):
     ref = outs[0].cpu().numpy()
     for u in outs[1:]:
         np.testing.assert_array_equal(u.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("name", ["p3_dyn", "p2_static_sep", "p2_planar_npsp", "p1_axis_dyn"])
+def test_plan_operand_views(fp, name):
+    """NearZonePlan.proj_op / interp_op / kernel_disp / seg_obs / seg_starts / d_er and
+    FarZonePlan.proj_op / interp_op (nearzone.py:55-80, farzone.py:32-44) read back from
+    the device plan: stencil starts and weights bit-identical to the oracle's
+    (grids.py:110-140), flat forms equal, the displacement table to round-off."""
+    from cases import SMALL_CASES, case_inputs, regime_of
+    from oracle.pipeline import build_plan as oracle_build
+    from oracle.problem import make_problem
+    case = SMALL_CASES[name]
+    pos, q, obs = case_inputs(name)
+    cfg = fp.PeriodicityConfig(dim=fp.Periodicity(case["dim"]), L=case["L"], k0=case["k0"],
+                               kshift=case["kshift"], regime=fp.Regime(regime_of(case)))
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = fp.build_plan(cfg, fp.TargetBox(case["D"]), fp.SourcePointSet(pos, q),
+                             fp.ObserverPointSet(pos if obs is None else obs), fp.SolverParams(**case["params"]))
+        ref = oracle_build(make_problem(case["dim"], L=case["L"], D=case["D"], k0=case["k0"],
+                                        kshift=case["kshift"], **case["params"]), pos, obs)
+    for got, want in ((plan.near.proj_op, ref.near.src), (plan.near.interp_op, ref.near.obs),
+                      (plan.far.proj_op, ref.far.src), (plan.far.interp_op, ref.far.obs)):
+        np.testing.assert_array_equal(got.axis_starts, want.starts)
+        for a in range(3):
+            np.testing.assert_array_equal(got.axis_weights[a], want.axis_w[a])
+        np.testing.assert_array_equal(got.flat_index, want.flat_index)
+        np.testing.assert_array_equal(got.flat_weight, want.flat_weight)
+        assert got.n_points == want.starts.shape[0] and got.stencil_size == want.flat_index.shape[1]
+    np.testing.assert_array_equal(plan.near.seg_obs, ref.near.seg_obs)
+    np.testing.assert_array_equal(plan.near.seg_starts, ref.near.seg_starts)
+    assert plan.near.kernel_disp.shape == ref.near.kernel_disp.shape
+    assert rel_l2(plan.near.kernel_disp, ref.near.kernel_disp) <= 1e-12
+    active = [a for a in range(3) if plan.near.grid.dims[a] > 1]
+    assert plan.near.d_er == case["params"].get("er_range_boxes", 1) * max(plan.near.grid.spacing[a] for a in active)
