@@ -21,9 +21,34 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.h"
 
 namespace {
+
+// NVTX ranges (FFTPIM_NVTX=1) around the C-ABI calls and the plan-build phases, for
+// nsys / ncu --nvtx timelines.  Header-only NVTX3: a no-op without a tool attached.
+struct NvtxRange {
+    bool on;
+    explicit NvtxRange(const char* name) {
+        static const bool enabled = [] {
+            const char* e = getenv("FFTPIM_NVTX");
+            return e && e[0] == '1';
+        }();
+        on = enabled;
+        if (on) nvtxRangePushA(name);
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+    void next(const char* name) {   // close the current phase, open the next
+        if (on) {
+            nvtxRangePop();
+            nvtxRangePushA(name);
+        }
+    }
+};
 
 thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
@@ -543,6 +568,7 @@ int64_t max_tile_count(FftpimPlan* P, const int* ocs, const double* d_obs, int64
 }
 
 void build(FftpimPlan* P) {
+    NvtxRange nv("fftpim build: sort, stencils, near kernel");
     const FftpimProblem& pr = P->prob;
     cudaStream_t s = P->build_stream;
     const int64_t N = pr.n_src, M = pr.n_obs;
@@ -698,6 +724,7 @@ void build(FftpimPlan* P) {
     P->obs_fstart = dalloc<int>(P, M * 3);
     launch_stencils(d_obs, P->obs_perm, M, P->far_og, P->obs_fw, P->obs_fstart, P->status, 23, s);
     check_status(P, "stencil construction");
+    nv.next("fftpim build: near kernel table, pair discovery");
     {
         // observer pass with stencils from sorted positions (line_kernels.cu) for
         // large observer sets; FFTPIM_OBS=pos|weights overrides
@@ -968,6 +995,7 @@ void build(FftpimPlan* P) {
     else   // far-zone-only plan: no correction pairs
         CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (Mown + 1), s));
     check_status(P, "correction pair discovery");
+    nv.next("fftpim build: pair coefficients, row order, K4 metadata");
     P->pair_ptr = dalloc<int64_t>(P, Mown + 1);
     {
         size_t bytes = 0;
@@ -1142,6 +1170,7 @@ void build(FftpimPlan* P) {
         }
     }
     check_status(P, "correction coefficients");
+    nv.next("fftpim build: K1 operator, far zone");
     CK(cudaStreamSynchronize(s));
     dfree(P, tables);
     dfree(P, counts);
@@ -2298,6 +2327,7 @@ static void sweep_evaluate(FftpimPlan* P, const double* q, double* u, cudaStream
 }
 
 int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* stream) {
+    NvtxRange nv("fftpim_sweep_evaluate");
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (!plan->sweep) return fail(Fail{FFTPIM_VALUE, "not a sweep plan (use fftpim_plan_evaluate)"});
     if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
@@ -2312,6 +2342,7 @@ int fftpim_sweep_evaluate(FftpimPlan* plan, const double* q, double* u, void* st
 }
 
 int fftpim_sweep_evaluate_host(FftpimPlan* plan, const double* q, double* u) {
+    NvtxRange nv("fftpim_sweep_evaluate_host");
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (!plan->sweep) return fail(Fail{FFTPIM_VALUE, "not a sweep plan (use fftpim_plan_evaluate_host)"});
     try {
@@ -2602,6 +2633,7 @@ int fftpim_group_create(const FftpimProblem* p, int32_t world, int32_t rank, con
 }
 
 int fftpim_group_evaluate(FftpimGroup* g, const double* q, double* u, void* stream) {
+    NvtxRange nv("fftpim_group_evaluate");
     if (!g || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (((uintptr_t)q | (uintptr_t)u) & 15) return fail(Fail{FFTPIM_VALUE, "q and u must be 16-byte aligned"});
     try {
@@ -2632,6 +2664,7 @@ void fftpim_group_destroy(FftpimGroup* g) {
 }
 
 int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts, void* stream) {
+    NvtxRange nv("fftpim_plan_evaluate");
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (plan->near_only && (parts & FFTPIM_FAR)) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
     if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});
@@ -2718,6 +2751,7 @@ static void staged_host_evaluate(FftpimPlan* P, const double* q, double* u, size
 }
 
 int fftpim_plan_evaluate_host(FftpimPlan* plan, const double* q, double* u, int64_t batch, int32_t parts) {
+    NvtxRange nv("fftpim_plan_evaluate_host");
     if (!plan || !q || !u) return fail(Fail{FFTPIM_VALUE, "null argument"});
     if (plan->near_only && (parts & FFTPIM_FAR)) return fail(Fail{FFTPIM_VALUE, "far-zone engine requires i_d >= 1"});
     if (plan->sweep) return fail(Fail{FFTPIM_VALUE, "sweep plans evaluate through fftpim_sweep_evaluate"});

@@ -75,6 +75,26 @@ def test_slab_group_w8_helmholtz_64_order4(fp):
     np.testing.assert_array_equal(grp.evaluate(q), u)
 
 
+def test_slab_group_c4_full_scale_emulated(fp):
+    """C4 at full scale (N = 8,388,608, 256^3, order 4, 6.1e9 pairs) decomposed into two
+    slab shards emulated on one GPU (61 GB of pairs each), against the reference's
+    own run on its seeded observer sample (tests/golden/c4_subset.npz)."""
+    import gc
+    import torch
+    from paper_2312_02376_b200.sharding import SlabGroup
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * 2**30:
+        pytest.skip("needs ~150 GB of free device memory")
+    cfg, box, src, obs, prm, q = _objs(fp, 4)
+    g = golden("c4_subset.npz")
+    grp = SlabGroup(cfg, box, src, obs, prm, world=2)
+    assert sum(int(i.n_pairs) for i in grp.infos) == 6105732016   # the single-domain plan's count
+    u = grp.evaluate(q)
+    assert rel_l2(u[g["obs_index"]], g["u"]) <= 1e-10
+    del grp
+    gc.collect()
+
+
 @pytest.mark.parametrize("c", [1, 2])
 def test_slab_group_nccl_single_rank(fp, c):
     """The NCCL code path itself (send/recv transposes, all-reduce, halo) with a

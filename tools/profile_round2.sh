@@ -3,8 +3,8 @@
 # test suite, smoke(), the default (C4) bench line with its composed CPU baseline,
 # the reference arm, bench lines for the other configs, the ncu launch list of the
 # default bench command, `--set full` captures of the evaluation kernels (C4),
-# the C3 K4 and the C5 sweep K4, and a compute-sanitizer memcheck pass over small
-# cases.  Each ncu pass runs only after the same command exited 0 without ncu.
+# the C3 K4 and the C5 sweep K4 (the .ncu-rep files stay in /tmp on the box; their raw
+# pages come back as CSV).  Each ncu pass runs only after the same command exited 0 without ncu.
 # Outputs land in gpurun_out/round2/.
 set -u
 OUT=gpurun_out/round2
@@ -27,14 +27,17 @@ if timeout 600 $CMD > $OUT/plain.log 2>&1; then
     -c 400 --csv --log-file $OUT/c4_launches.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
   timeout 1500 ncu --set full --clock-control none --import-source on \
     -k regex:"k_corr_tiles|k_k1_lines|k_observers|k_fft_reg|k_far_project|k_permute_q" -s 9 -c 10 \
-    -o $OUT/c4_full $CMD > $OUT/ncu_c4_full.log 2>&1; echo "ncu c4 full rc=$?"
+    -f -o /tmp/c4_full $CMD > $OUT/ncu_c4_full.log 2>&1; echo "ncu c4 full rc=$?"
+  ncu -i /tmp/c4_full.ncu-rep --page raw --csv > $OUT/c4_full_raw.csv 2>/dev/null
 fi
-CMD3="python bench.py --config 3 --steps 1 --warmup 3 --no-cpu-baseline"
-timeout 1200 ncu --set full --clock-control none -k regex:"k_corr_tiles|k_k1_spmv|k_observers|k_far_project" -s 8 -c 4 \
-    -o $OUT/c3_full $CMD3 > $OUT/ncu_c3_full.log 2>&1; echo "ncu c3 full rc=$?"
+CMD3="python bench.py --config 3 --steps 1 --warmup 2 --no-cpu-baseline"
+# C3 holds 172 GB: a multi-pass --set full capture cannot save/restore device memory, so
+# the single-pass launch list (time + DRAM bytes per launch) stands in for it
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -c 300 --csv --log-file $OUT/c3_launches.csv $CMD3 > $OUT/ncu_c3_launches.log 2>&1; echo "ncu c3 launches rc=$?"
 CMD5="python bench.py --config 5 --steps 1 --warmup 2 --no-cpu-baseline"
 unset FFTPIM_NO_GRAPHS
 timeout 1200 ncu --set full --clock-control none -k regex:"k_corr_sweep" -s 1 -c 1 \
-    -o $OUT/c5_sweep $CMD5 > $OUT/ncu_c5_sweep.log 2>&1; echo "ncu c5 sweep rc=$?"
-timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 3 python -m pytest tests/test_gpu_parity.py -q -x \
-    -k "test_small_case_parity and (p3_dyn or p1_dyn or p2_npsp_o4 or p3_npsp)" > $OUT/sanitizer_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -4 $OUT/sanitizer_memcheck.log
+    -f -o /tmp/c5_sweep $CMD5 > $OUT/ncu_c5_sweep.log 2>&1; echo "ncu c5 sweep rc=$?"
+ncu -i /tmp/c5_sweep.ncu-rep --page raw --csv > $OUT/c5_sweep_raw.csv 2>/dev/null
+# compute-sanitizer is closed on this pool (gpurun refuses it): not run.
