@@ -115,14 +115,24 @@ def stage_bytes(w, info, n_far):
     nfft = int(np.prod(info.fft_dims))
     P = int(info.n_pairs)
     sc = 8 if info.real_coefficients else 16
+    n0, n1, n2 = (int(v) for v in info.near_dims)
+    L0, L1, L2 = (int(v) for v in info.fft_dims)
+    a1, a2 = n0 * n1 * L2, n0 * L1 * L2
+    fold = 1.0
+    for ax in (1, 2):   # G_near is even along an axis without a phase shift (fftpim.cu: fold_y / fold_z)
+        if info.near_dims[ax] > 1 and (ax >= w.dim or w.kshift[ax] == 0):
+            fold *= 0.5
     return {
         "permute_q": 16 * N + 4 * N + 16 * N,
         "far_project": N * (24 + 16) + 16 * n_far,
         # positions + q read, the n^3 grid written once (the pruned FFT never stores the padding)
         "near_project": N * (24 + 16) + 16 * ng,
-        "fft_forward": 2 * 16 * nfft,
-        "spectrum_mul": 3 * 16 * nfft,
-        "fft_inverse": 2 * 16 * nfft,
+        # pruned column stages (K2): the zero padding is never stored.  z: n^3 -> n0 n1 L2,
+        # y: -> n0 L1 L2; fused x stage in place on n0 L1 L2 plus the spectrum, read at its folded
+        # columns (half per even axis); the inverse mirrors the forward stages
+        "fft_forward": 16 * (ng + 2 * a1 + a2),
+        "spectrum_mul": 16 * 2 * a2 + int(16 * nfft * fold),
+        "fft_inverse": 16 * (ng + 2 * a1 + a2),
         # K4: coefficient + int32 source index per pair, q gathered once, row sums out
         "corr_matvec": P * (sc + 4) + 16 * N + 16 * M,
         # K3 + K5c + fix-up: observer stencil, grid reads, row sums, u written once

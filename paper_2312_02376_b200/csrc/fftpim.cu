@@ -1353,6 +1353,8 @@ void build(FftpimPlan* P) {
                 const int64_t nch = (nfp + far_win_chunk(nfp) - 1) / far_win_chunk(nfp);
                 P->far_slots = dalloc<cplx>(P, std::max<int64_t>(nch, 1) * nf);
                 P->far_win = dalloc<int>(P, std::max<int64_t>(nch, 1) * 6);
+                // the windows depend on the positions only: computed once here
+                launch_far_win_bounds(P->far_sg, P->src_pos_s + 3 * (P->sharded ? P->i0 : 0), nfp, P->far_win, s);
             }
         }
         P->far_qg = dalloc<cplx>(P, nf);

@@ -188,6 +188,7 @@ void launch_gather_pos(const double* pos, const int* perm, int64_t n, double* ou
 bool launch_observers_pos(const EvalArgs& a, const double* pos, cudaStream_t s, int mode);
 bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, int* win, cudaStream_t s);
 int far_win_chunk(int64_t n);
+void launch_far_win_bounds(const StencilGeom& fs, const double* pos, int64_t n, int* win, cudaStream_t s);
 int64_t launch_max_tile_count(const StencilGeom& g, const int* ocs, cudaStream_t s);
 bool launch_observers_tile(const EvalArgs& a, const double* pos, const int* ocs, int64_t i0, cudaStream_t s,
                            int mode);

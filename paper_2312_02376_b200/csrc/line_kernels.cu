@@ -1053,6 +1053,149 @@ __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, 
     }
 }
 
+// Plan-time bounding windows of the chunks (the positions never change): pass 1
+// of k_far_project_win once, so that the evaluation kernel below starts at pass 2.
+template <int WF>
+__global__ void __launch_bounds__(256) k_far_win_bounds(StencilGeom fs, FarWinArgs f) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + warp;
+    if (c >= f.nchunks) return;
+    const int64_t p0 = (int64_t)c * f.chunk, p1 = min(p0 + f.chunk, f.n);
+    const LagrangeDen<WF> L;
+    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-1, -1, -1};
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            double w[WF];
+            const int s = fast_stencil<WF>(__ldg(f.pos + 3 * p + ax), fs.n[ax], fs.origin[ax], fs.h[ax], f.rf[ax], L, w);
+            lo[ax] = min(lo[ax], s);
+            hi[ax] = max(hi[ax], s);
+        }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax)
+        for (int o = 16; o; o >>= 1) {
+            lo[ax] = min(lo[ax], __shfl_xor_sync(0xffffffffu, lo[ax], o));
+            hi[ax] = max(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], o));
+        }
+    if (lane < 3) {
+        f.win[6 * c + lane] = lo[lane];
+        f.win[6 * c + 3 + lane] = min(hi[lane] + fs.w[lane], fs.n[lane]) - lo[lane];
+    }
+}
+
+// k_far_project_win with the windows read from the plan (no pass 1) and the
+// batch of 32 staged points split into runs of equal stencil starts by one
+// ballot: the inner loop over a run has no data-dependent branch, so the
+// shared-memory loads of the following points are in flight while a point's
+// products retire.  Same chunks, runs and summation order as k_far_project_win:
+// the far grid is bit-identical.
+template <int WF>
+__global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win2(EvalArgs a, FarWinArgs f) {
+    constexpr int TPL = (WF * WF * WF + 31) / 32;
+    constexpr int REC = 3 * WF + 2;
+    extern __shared__ double fpw_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * FPW_WARPS + warp;
+    if (c >= f.nchunks) return;
+    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * FPW_CAP;
+    double* stage = fpw_smem + 2 * FPW_WARPS * FPW_CAP + warp * 32 * REC;
+    const StencilGeom& fs = a.fs;
+    const int nf = fs.n[0] * fs.n[1] * fs.n[2];
+    const int64_t p0 = (int64_t)c * f.chunk, p1 = min(p0 + f.chunk, f.n);
+    const LagrangeDen<WF> L;
+    const int lo0 = __ldg(f.win + 6 * c), lo1 = __ldg(f.win + 6 * c + 1), lo2 = __ldg(f.win + 6 * c + 2);
+    const int ext0 = __ldg(f.win + 6 * c + 3), ext1 = __ldg(f.win + 6 * c + 4), ext2 = __ldg(f.win + 6 * c + 5);
+    const int wn = ext0 * ext1 * ext2;
+    const bool in_smem = wn <= FPW_CAP;
+    cplx* dst = in_smem ? wgrid : f.slots + (int64_t)c * nf;
+    for (int t = lane; t < wn; t += 32) dst[t] = mk(0.0);
+    // this lane's taps: word offsets into a staged record and into the window
+    int oa[TPL], ob[TPL], oc[TPL], od[TPL];
+    bool tok[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) {
+        const int tp = lane + 32 * t;
+        const int tc = tp % WF, tb = (tp / WF) % WF, ta = tp / (WF * WF);
+        tok[t] = tp < WF * WF * WF && ta < fs.w[0] && tb < fs.w[1] && tc < fs.w[2];
+        oa[t] = tok[t] ? ta : 0;
+        ob[t] = tok[t] ? WF + tb : WF;
+        oc[t] = tok[t] ? 2 * WF + tc : 2 * WF;
+        od[t] = (ta * ext1 + tb) * ext2 + tc;
+    }
+    double accr[TPL], acci[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) accr[t] = acci[t] = 0.0;
+    int c0 = -1, c1 = 0, c2 = 0;
+    auto flush = [&]() {
+        const int base = ((c0 - lo0) * ext1 + (c1 - lo1)) * ext2 + (c2 - lo2);
+#pragma unroll
+        for (int t = 0; t < TPL; ++t) {
+            if (!tok[t]) continue;
+            cplx& d = dst[base + od[t]];
+            d.re += accr[t];
+            d.im += acci[t];
+            accr[t] = acci[t] = 0.0;
+        }
+        __syncwarp();
+    };
+    __syncwarp();
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int64_t p = base + lane;
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int s0 = c0, s1 = c1, s2 = c2;
+        __syncwarp();
+        if (p < p1) {
+            double* r = stage + lane * REC;
+            s0 = fast_stencil<WF>(__ldg(f.pos + 3 * p), fs.n[0], fs.origin[0], fs.h[0], f.rf[0], L, r);
+            s1 = fast_stencil<WF>(__ldg(f.pos + 3 * p + 1), fs.n[1], fs.origin[1], fs.h[1], f.rf[1], L, r + WF);
+            s2 = fast_stencil<WF>(__ldg(f.pos + 3 * p + 2), fs.n[2], fs.origin[2], fs.h[2], f.rf[2], L, r + 2 * WF);
+            const double2 qv = __ldg(reinterpret_cast<const double2*>(f.q + p));
+            r[3 * WF] = qv.x;
+            r[3 * WF + 1] = qv.y;
+        }
+        // run heads: a staged point whose start differs from its predecessor's
+        // (lane 0: from the start carried over from the previous batch)
+        int q0 = __shfl_up_sync(0xffffffffu, s0, 1), q1 = __shfl_up_sync(0xffffffffu, s1, 1),
+            q2 = __shfl_up_sync(0xffffffffu, s2, 1);
+        if (lane == 0) {
+            q0 = c0;
+            q1 = c1;
+            q2 = c2;
+        }
+        const unsigned heads = __ballot_sync(0xffffffffu, lane < cnt && (s0 != q0 || s1 != q1 || s2 != q2));
+        __syncwarp();
+        int j = 0;
+        while (j < cnt) {
+            if ((heads >> j) & 1u) {
+                if (c0 >= 0) flush();
+                c0 = __shfl_sync(0xffffffffu, s0, j);
+                c1 = __shfl_sync(0xffffffffu, s1, j);
+                c2 = __shfl_sync(0xffffffffu, s2, j);
+            }
+            const unsigned rest = j < 31 ? heads & (0xffffffffu << (j + 1)) : 0u;
+            const int e = rest ? __ffs(rest) - 1 : cnt;
+#pragma unroll 4
+            for (int k = j; k < e; ++k) {
+                const double* r = stage + k * REC;
+                const double qre = r[3 * WF], qim = r[3 * WF + 1];
+#pragma unroll
+                for (int t = 0; t < TPL; ++t) {
+                    const double wgt = (r[oa[t]] * r[ob[t]]) * r[oc[t]];
+                    accr[t] += wgt * qre;
+                    acci[t] += wgt * qim;
+                }
+            }
+            j = e;
+        }
+    }
+    if (c0 >= 0) flush();
+    if (in_smem) {
+        cplx* out = f.slots + (int64_t)c * nf;
+        for (int t = lane; t < wn; t += 32) out[t] = wgrid[t];
+    }
+}
+
 // far node t: sum of the chunk windows covering it, chunks in a fixed tree order
 __global__ void __launch_bounds__(256) k_far_windows_reduce(FarWinArgs f, int nfx, int nfy, int nfz, cplx* qg) {
     const int t = blockIdx.x;
@@ -1081,6 +1224,28 @@ int far_win_chunk(int64_t n) {
     return (int)((c + 31) / 32 * 32);
 }
 
+// plan build: the chunk windows of n sorted points (read by k_far_project_win2)
+void launch_far_win_bounds(const StencilGeom& fs, const double* pos, int64_t n, int* win, cudaStream_t s) {
+    if (!pos || !win || n <= 0) return;
+    FarWinArgs f;
+    f.pos = pos;
+    f.q = nullptr;
+    f.n = n;
+    f.chunk = far_win_chunk(n);
+    f.nchunks = (int)((n + f.chunk - 1) / f.chunk);
+    f.slots = nullptr;
+    f.win = win;
+    for (int ax = 0; ax < 3; ++ax) f.rf[ax] = fs.h[ax] > 0 ? 1.0 / fs.h[ax] : 0.0;
+    const int blocks = (f.nchunks + 7) / 8;
+    switch (fs.order + 1) {
+        case 3: k_far_win_bounds<3><<<blocks, 256, 0, s>>>(fs, f); break;
+        case 4: k_far_win_bounds<4><<<blocks, 256, 0, s>>>(fs, f); break;
+        case 5: k_far_win_bounds<5><<<blocks, 256, 0, s>>>(fs, f); break;
+        default: return;
+    }
+    fftpim_count_launch();
+}
+
 bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, int* win, cudaStream_t s) {
     if (!pos || !slots) return false;
     FarWinArgs f;
@@ -1096,18 +1261,28 @@ bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, i
     const size_t smem = (size_t)FPW_WARPS * (FPW_CAP * sizeof(cplx) + 32 * (3 * WF + 2) * sizeof(double) +
                                              32 * 3 * sizeof(int));
     const int blocks = (f.nchunks + FPW_WARPS - 1) / FPW_WARPS;
-    auto go = [&](auto kern) {
+    // FFTPIM_FAR_WIN2=0: the round-2a kernel that recomputes the windows every evaluation
+    static const bool v2 = [] {
+        const char* e = getenv("FFTPIM_FAR_WIN2");
+        return !(e && e[0] == '0');
+    }();
+    auto go = [&](auto kern, auto kern2) {
         static size_t configured = 48 * 1024;
         if (smem > configured) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             configured = smem;
         }
-        if (f.nchunks > 0) kern<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
+        if (f.nchunks <= 0) return;
+        if (v2)
+            kern2<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
+        else
+            kern<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
     };
     switch (WF) {
-        case 3: go(k_far_project_win<3>); break;
-        case 4: go(k_far_project_win<4>); break;
-        case 5: go(k_far_project_win<5>); break;
+        case 3: go(k_far_project_win<3>, k_far_project_win2<3>); break;
+        case 4: go(k_far_project_win<4>, k_far_project_win2<4>); break;
+        case 5: go(k_far_project_win<5>, k_far_project_win2<5>); break;
         default: return false;
     }
     const int nf = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];

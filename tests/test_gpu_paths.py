@@ -82,6 +82,20 @@ def test_k4_16bit_offsets_bitwise(case, tmp_path):
     np.testing.assert_array_equal(u16, u32)
 
 
+@pytest.mark.parametrize("case", ["c2", "blobs3d", "p2_planar_npsp", "p1_axis_dyn", "p3_dyn"])
+def test_far_windows_from_the_plan_bitwise(case, tmp_path):
+    """Windowed far projection reading the plan-time chunk windows and splitting
+    staged batches into runs by ballot (k_far_project_win2) against the kernel
+    that recomputes the windows and tests every point (k_far_project_win): same
+    chunks, runs and summation order -> identical bits; both within rounding of
+    the stored-weight projection."""
+    u2, _ = run_variant(case, {"FFTPIM_FAR": "win"}, tmp_path, "win2")
+    u1, _ = run_variant(case, {"FFTPIM_FAR": "win", "FFTPIM_FAR_WIN2": "0"}, tmp_path, "win1")
+    uw, _ = run_variant(case, {"FFTPIM_FAR": "warps"}, tmp_path, "warps")
+    np.testing.assert_array_equal(u2, u1)
+    assert rel_l2(u2, uw) <= 1e-13
+
+
 def test_pageable_host_entry_staged():
     """Pageable caller buffers above 8 MiB go through the plan's pinned staging in
     chunks (host threads copying beside the DMA): bitwise equal to the device
