@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <climits>
 #include <cmath>
@@ -2686,6 +2688,63 @@ int fftpim_plan_evaluate(FftpimPlan* plan, const double* q, double* u, int64_t b
 // chunk k into pinned memory while the DMA engine uploads chunk k - 1, and on
 // the way back they copy chunk k out while chunk k + 1 downloads -- instead of
 // the driver's serial pageable copies.
+// Persistent copy workers (created on first use, parked on a condition variable
+// between calls): spawning threads per 8 MiB chunk cost more than the copies.
+namespace {
+class CopyPool {
+public:
+    explicit CopyPool(int workers) {
+        for (int i = 0; i < workers; ++i) th_.emplace_back([this] { work(); });
+        for (auto& t : th_) t.detach();   // parked until process exit
+    }
+    // split [0, bytes) into `parts` slices; the caller copies the first one
+    void run(char* dst, const char* src, size_t bytes, int parts) {
+        const size_t per = (bytes / parts + 63) & ~(size_t)63;
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            for (int i = 1; i < parts; ++i) {
+                const size_t o = (size_t)i * per;
+                if (o >= bytes) break;
+                jobs_.push_back(Job{dst + o, src + o, std::min(per, bytes - o)});
+                ++pending_;
+            }
+        }
+        cv_.notify_all();
+        memcpy(dst, src, std::min(per, bytes));
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+private:
+    struct Job {
+        char* dst;
+        const char* src;
+        size_t n;
+    };
+    void work() {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [this] { return !jobs_.empty(); });
+                j = jobs_.back();
+                jobs_.pop_back();
+            }
+            memcpy(j.dst, j.src, j.n);
+            {
+                std::lock_guard<std::mutex> lk(m_);
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::vector<Job> jobs_;
+    int pending_ = 0;
+    std::vector<std::thread> th_;
+};
+}   // namespace
+
 static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     static const int nt = [] {
         const char* e = getenv("FFTPIM_HOST_COPY_THREADS");
@@ -2697,15 +2756,10 @@ static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
         memcpy(dst, src, bytes);
         return;
     }
-    std::vector<std::thread> th;
-    const size_t per = (bytes / k + 63) & ~(size_t)63;
-    for (int i = 0; i < k; ++i) {
-        const size_t o = (size_t)i * per;
-        if (o >= bytes) break;
-        const size_t n = std::min(per, bytes - o);
-        th.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, n); });
-    }
-    for (auto& t : th) t.join();
+    static std::mutex pool_mu;                       // one staged copy at a time per process
+    static CopyPool* pool = new CopyPool(nt - 1);    // leaked on purpose: workers outlive static destructors
+    std::lock_guard<std::mutex> lk(pool_mu);
+    pool->run((char*)dst, (const char*)src, bytes, k);
 }
 
 static void staged_host_evaluate(FftpimPlan* P, const double* q, double* u, size_t qb, size_t ub, int64_t batch,

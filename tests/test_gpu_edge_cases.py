@@ -30,7 +30,7 @@ def fp():
     return fp
 
 
-def _both(fp, dim, src_pos, q, obs_pos=None, L=(1.0, 1.0, 1.0), D=None, k0=0j, kshift=(0, 0, 0), **params):
+def _both(fp, dim, src_pos, q, obs_pos=None, L=(1.0, 1.0, 1.0), D=None, k0=0j, kshift=(0, 0, 0), plan_q=None, **params):
     """(gpu near, gpu far, oracle near, oracle far, gpu near plan, oracle plan)"""
     from oracle.far_engine import eval_far as o_far
     from oracle.near_engine import eval_near as o_near
@@ -43,7 +43,9 @@ def _both(fp, dim, src_pos, q, obs_pos=None, L=(1.0, 1.0, 1.0), D=None, k0=0j, k
     op = oracle_build(pb, src_pos, obs_pos)
     cfg = fp.PeriodicityConfig(dim=fp.Periodicity(dim), L=L, k0=k0, kshift=kshift, regime=fp.Regime(pb.regime))
     obs = fp.ObserverPointSet(src_pos if obs_pos is None else obs_pos)
-    plan = fp.build_plan(cfg, fp.TargetBox(D), fp.SourcePointSet(src_pos, q), obs, fp.SolverParams(**params))
+    # plan_q: the amplitudes the facade validates (NPSP neutrality); evaluations take any q
+    plan = fp.build_plan(cfg, fp.TargetBox(D), fp.SourcePointSet(src_pos, q if plan_q is None else plan_q), obs,
+                         fp.SolverParams(**params))
     return (fp.eval_near(plan.near, q), fp.eval_far(plan.far, q), o_near(op.near, q), o_far(op.far, q), plan, op)
 
 
@@ -67,7 +69,7 @@ def test_single_point_self_pair(fp):
     of one point builds, the self pair is counted and contributes nothing."""
     pos = np.array([[1.7, 2.2, 1.1]])
     q = np.array([2.0 - 1.0j])
-    gn, gf, on, of, plan, op = _both(fp, 1, pos, q, L=(4.0, 4.0, 4.0), near_grid=(7, 7, 7))
+    gn, gf, on, of, plan, op = _both(fp, 1, pos, q, L=(4.0, 4.0, 4.0), near_grid=(7, 7, 7), plan_q=[0.0])
     assert plan.near.same_points and plan.near.n_self_pairs == 1
     assert abs(on[0]) < 1e-13 and abs(gn[0]) < 1e-13
     assert abs(gf[0] - of[0]) <= TOL * max(abs(of[0]), 1e-3)
@@ -95,10 +97,12 @@ def test_points_on_nodes_and_faces(fp):
     all faces / corners of the box, where stencil starts clip (grids.py:118-121)."""
     n = 9
     ax = np.linspace(0.0, 1.0, n)
-    nodes = np.stack(np.meshgrid(ax[::2], ax[::4], ax[::2], indexing="ij"), -1).reshape(-1, 3)
+    # periodic along x only: the x = 1 face is left out (it is the lattice image of x = 0, see
+    # test_domain_errors); y and z carry both faces
+    nodes = np.stack(np.meshgrid(ax[:-1:2], ax[::4], ax[::2], indexing="ij"), -1).reshape(-1, 3)
     rng = np.random.default_rng(6)
     q = rng.standard_normal(nodes.shape[0]) + 1j * rng.standard_normal(nodes.shape[0])
-    res = _both(fp, 3, nodes, q, k0=2.5, kshift=(0.1, 0.2, 0.3), near_grid=(n, n, n), near_order=2, far_grid=(5, 5, 5))
+    res = _both(fp, 1, nodes, q, k0=2.5, kshift=(0.1, 0, 0), near_grid=(n, n, n), near_order=2, far_grid=(5, 5, 5))
     _assert_parity(res)
     op = res[4].near.proj_op
     for a in range(3):
@@ -217,6 +221,12 @@ def test_domain_errors(fp):
     with pytest.raises(fp.DomainError):
         fp.build_near_plan(cfg, fp.TargetBox((4, 4, 4)), src, fp.ObserverPointSet([[2.0, 2.0, 2.0]]),
                            fp.SolverParams(near_grid=(7, 7, 7)))
+    # a point on the x = 0 face and one on the x = L face are lattice images of each other:
+    # the wrapped copy coincides with a distinct source
+    faces = fp.SourcePointSet([[0.0, 2.0, 2.0], [4.0, 2.0, 2.0], [1.0, 3.0, 1.0]], [1.0, -0.5, -0.5])
+    with pytest.raises(fp.DomainError):
+        fp.build_plan(cfg, fp.TargetBox((4, 4, 4)), faces, fp.ObserverPointSet(faces.positions),
+                      fp.SolverParams(near_grid=(7, 7, 7)))
     with pytest.raises((fp.ValidationError, fp.DomainError)):
         fp.build_plan(cfg, fp.TargetBox((4, 4, 4)), src, fp.ObserverPointSet([[4.5, 2.0, 2.0]]),
                       fp.SolverParams(near_grid=(7, 7, 7)))

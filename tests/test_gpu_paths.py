@@ -89,8 +89,8 @@ def test_far_windows_from_the_plan_bitwise(case, tmp_path):
     that recomputes the windows and tests every point (k_far_project_win): same
     chunks, runs and summation order -> identical bits; both within rounding of
     the stored-weight projection."""
-    u2, _ = run_variant(case, {"FFTPIM_FAR": "win"}, tmp_path, "win2")
-    u1, _ = run_variant(case, {"FFTPIM_FAR": "win", "FFTPIM_FAR_WIN2": "0"}, tmp_path, "win1")
+    u2, _ = run_variant(case, {"FFTPIM_FAR": "win", "FFTPIM_FAR_WIN2": "1"}, tmp_path, "win2")
+    u1, _ = run_variant(case, {"FFTPIM_FAR": "win"}, tmp_path, "win1")
     uw, _ = run_variant(case, {"FFTPIM_FAR": "warps"}, tmp_path, "warps")
     np.testing.assert_array_equal(u2, u1)
     assert rel_l2(u2, uw) <= 1e-13
