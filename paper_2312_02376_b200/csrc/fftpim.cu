@@ -1352,11 +1352,12 @@ void build(FftpimPlan* P) {
                     launch_gather_pos(d_src, P->src_perm, N, P->src_pos_s, s);
                 }
                 const int64_t nfp = P->sharded ? Mown : N;   // points the far projection takes
-                const int64_t nch = (nfp + far_win_chunk(nfp) - 1) / far_win_chunk(nfp);
+                // chunk length, window capacity and the chunk windows depend on the positions only
+                P->far_win = dalloc<int>(P, far_win_max_chunks(nfp) * 6);
+                far_win_setup(P->far_sg, P->src_pos_s + 3 * (P->sharded ? P->i0 : 0), nfp, P->far_win, &P->far_chunk,
+                              &P->far_cap, s);
+                const int64_t nch = (nfp + P->far_chunk - 1) / P->far_chunk;
                 P->far_slots = dalloc<cplx>(P, std::max<int64_t>(nch, 1) * nf);
-                P->far_win = dalloc<int>(P, std::max<int64_t>(nch, 1) * 6);
-                // the windows depend on the positions only: computed once here
-                launch_far_win_bounds(P->far_sg, P->src_pos_s + 3 * (P->sharded ? P->i0 : 0), nfp, P->far_win, s);
             }
         }
         P->far_qg = dalloc<cplx>(P, nf);
@@ -1452,6 +1453,8 @@ EvalArgs eval_args(FftpimPlan* P, const double* q, double* u, int parts) {
     a.far_pos = P->far_slots ? P->src_pos_s : nullptr;
     a.far_slots = P->far_slots;
     a.far_win = P->far_win;
+    a.far_chunk = P->far_chunk;
+    a.far_cap = P->far_cap;
     a.k1_scratch = P->k1_scratch;
     a.k1_cnt = P->k1_cnt;
     a.k1_row = P->k1_row;

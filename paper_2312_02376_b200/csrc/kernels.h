@@ -164,6 +164,7 @@ struct EvalArgs {
     const double* far_pos;      // their sorted positions (non-null: windowed far projection)
     cplx* far_slots;            // windowed far projection: per-chunk windows
     int* far_win;
+    int far_chunk, far_cap;     // points per warp chunk, shared-memory window entries per warp
     int64_t far_n;
     cplx* obs_pre;              // far + K4 fix-up per sorted observer (split observer pass)
     cplx* u_sorted;             // grid-tile observer pass: store near + far here in sorted order (no K4 term)
@@ -187,8 +188,9 @@ void launch_stencil_records(const double* w, const int* start, int64_t n, int W,
 void launch_gather_pos(const double* pos, const int* perm, int64_t n, double* out, cudaStream_t s);
 bool launch_observers_pos(const EvalArgs& a, const double* pos, cudaStream_t s, int mode);
 bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, int* win, cudaStream_t s);
-int far_win_chunk(int64_t n);
-void launch_far_win_bounds(const StencilGeom& fs, const double* pos, int64_t n, int* win, cudaStream_t s);
+int64_t far_win_max_chunks(int64_t n);
+void far_win_setup(const StencilGeom& fs, const double* pos, int64_t n, int* win, int* chunk_out, int* cap_out,
+                   cudaStream_t s);
 int64_t launch_max_tile_count(const StencilGeom& g, const int* ocs, cudaStream_t s);
 bool launch_observers_tile(const EvalArgs& a, const double* pos, const int* ocs, int64_t i0, cudaStream_t s,
                            int mode);

@@ -76,9 +76,18 @@ __device__ __forceinline__ int fast_stencil(double x, int n, double origin, doub
     return s;
 }
 
+#ifndef K1L_TY
 #define K1L_TY 16
+#endif
+#ifndef K1L_TZ
 #define K1L_TZ 32
-#define K1L_R 4
+#endif
+#ifndef K1L_R
+#define K1L_R 4     // z lines per thread
+#endif
+#ifndef K1L_MINB
+#define K1L_MINB 3  // resident blocks per SM the register budget is set for
+#endif
 #define K1L_NT (K1L_TY * (K1L_TZ / K1L_R))
 
 template <int W>
@@ -94,9 +103,11 @@ size_t k1_lines_smem(int cap) {
     return (size_t)cap * T::REC * sizeof(double) + (size_t)(2 * T::ROWS * (T::CELLS + 1) + T::ROWS + 1) * sizeof(int);
 }
 
+#ifndef K1L_PF
 #define K1L_PF 3   // staged points per thread per piece held in flight (cap <= K1L_PF * K1L_NT)
+#endif
 template <int W>
-__global__ void __launch_bounds__(K1L_NT, 3) k_k1_lines(EvalArgs a, const double* __restrict__ pos, int xc,
+__global__ void __launch_bounds__(K1L_NT, K1L_MINB) k_k1_lines(EvalArgs a, const double* __restrict__ pos, int xc,
                                                         int n_items, int cap, double rh0, double rh1, double rh2) {
     using T = K1Lines<W>;
     constexpr int ROWS = T::ROWS, CELLS = T::CELLS, REC = T::REC, R = K1L_R, LCS = ROWS * (CELLS + 1);
@@ -929,13 +940,14 @@ bool launch_observers_tile(const EvalArgs& a, const double* pos, const int* ocs,
 // The chunk windows are then summed per far node in a fixed order
 // (k_far_windows_reduce): no atomics, bitwise reproducible.
 #define FPW_WARPS 8
-#define FPW_CAP 400
+#define FPW_CAP 400       // window entries per warp in shared memory: 400 (2 blocks per SM) or 256 (3 blocks)
 struct FarWinArgs {
     const double* pos;          // sorted positions of the projected points
     const cplx* q;              // their sorted charges
     int64_t n;                  // points
     int chunk;                  // points per warp chunk
     int nchunks;
+    int cap;                    // shared-memory window entries per warp
     cplx* slots;                // (nchunks, nf) windows
     int* win;                   // (nchunks, 6): x0, y0, z0, ex, ey, ez
     double rf[3];
@@ -945,13 +957,13 @@ template <int WF>
 __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, FarWinArgs f) {
     constexpr int TPL = (WF * WF * WF + 31) / 32;
     constexpr int REC = 3 * WF + 2;
-    extern __shared__ double fpw_smem[];
+    extern __shared__ __align__(16) double fpw_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * FPW_WARPS + warp;
     if (c >= f.nchunks) return;
-    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * FPW_CAP;
-    double* stage = fpw_smem + 2 * FPW_WARPS * FPW_CAP + warp * 32 * REC;
-    int* sst = reinterpret_cast<int*>(fpw_smem + 2 * FPW_WARPS * FPW_CAP + FPW_WARPS * 32 * REC) + warp * 32 * 3;
+    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * f.cap;
+    double* stage = fpw_smem + 2 * FPW_WARPS * f.cap + warp * 32 * REC;
+    int* sst = reinterpret_cast<int*>(fpw_smem + 2 * FPW_WARPS * f.cap + FPW_WARPS * 32 * REC) + warp * 32 * 3;
     const StencilGeom& fs = a.fs;
     const int nfx = fs.n[0], nfy = fs.n[1], nfz = fs.n[2];
     const int nf = nfx * nfy * nfz;
@@ -978,7 +990,7 @@ __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win(EvalArgs a, 
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) ext[ax] = min(hi[ax] + fs.w[ax], fs.n[ax]) - lo[ax];
     const int wn = ext[0] * ext[1] * ext[2];
-    const bool in_smem = wn <= FPW_CAP;
+    const bool in_smem = wn <= f.cap;
     cplx* dst = in_smem ? wgrid : f.slots + (int64_t)c * nf;
     for (int t = lane; t < wn; t += 32) dst[t] = mk(0.0);
     if (lane < 3) {
@@ -1094,12 +1106,12 @@ template <int WF>
 __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win2(EvalArgs a, FarWinArgs f) {
     constexpr int TPL = (WF * WF * WF + 31) / 32;
     constexpr int REC = 3 * WF + 2;
-    extern __shared__ double fpw_smem[];
+    extern __shared__ __align__(16) double fpw_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * FPW_WARPS + warp;
     if (c >= f.nchunks) return;
-    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * FPW_CAP;
-    double* stage = fpw_smem + 2 * FPW_WARPS * FPW_CAP + warp * 32 * REC;
+    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * f.cap;
+    double* stage = fpw_smem + 2 * FPW_WARPS * f.cap + warp * 32 * REC;
     const StencilGeom& fs = a.fs;
     const int nf = fs.n[0] * fs.n[1] * fs.n[2];
     const int64_t p0 = (int64_t)c * f.chunk, p1 = min(p0 + f.chunk, f.n);
@@ -1107,7 +1119,7 @@ __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win2(EvalArgs a,
     const int lo0 = __ldg(f.win + 6 * c), lo1 = __ldg(f.win + 6 * c + 1), lo2 = __ldg(f.win + 6 * c + 2);
     const int ext0 = __ldg(f.win + 6 * c + 3), ext1 = __ldg(f.win + 6 * c + 4), ext2 = __ldg(f.win + 6 * c + 5);
     const int wn = ext0 * ext1 * ext2;
-    const bool in_smem = wn <= FPW_CAP;
+    const bool in_smem = wn <= f.cap;
     cplx* dst = in_smem ? wgrid : f.slots + (int64_t)c * nf;
     for (int t = lane; t < wn; t += 32) dst[t] = mk(0.0);
     // this lane's taps: word offsets into a staged record and into the window
@@ -1196,6 +1208,132 @@ __global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win2(EvalArgs a,
     }
 }
 
+// Order-3 far stencils (4^3 = 64 taps), four staged points per warp step: the warp
+// splits into four groups of 8 lanes, group g takes point a + 4 r + g of a run
+// [a, b) of equal stencil starts, and a lane owns the 8 taps (ta = 0..3,
+// tb = 2 h, 2 h + 1, tc) with h = (lane & 7) >> 2, tc = lane & 3: five
+// shared-memory loads (two 16-byte wx pairs, one wy pair, wz, q) feed 32 FP64
+// instructions, ~10 instructions per point instead of ~25.  At the end of a run
+// the four groups' sums are added by two shuffle steps in a fixed order and
+// group g adds the taps ta = g to the window.  Windows, chunks and runs as in
+// k_far_project_win2; the sums differ from k_far_project_win's in the last bits
+// only (another fixed order).
+__global__ void __launch_bounds__(32 * FPW_WARPS) k_far_project_win4(EvalArgs a, FarWinArgs f) {
+    constexpr int WF = 4, REC = 3 * WF + 2;
+    extern __shared__ __align__(16) double fpw_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * FPW_WARPS + warp;
+    if (c >= f.nchunks) return;
+    cplx* wgrid = reinterpret_cast<cplx*>(fpw_smem) + warp * f.cap;
+    double* stage = fpw_smem + 2 * FPW_WARPS * f.cap + warp * 32 * REC;
+    const StencilGeom& fs = a.fs;
+    const int nf = fs.n[0] * fs.n[1] * fs.n[2];
+    const int64_t p0 = (int64_t)c * f.chunk, p1 = min(p0 + f.chunk, f.n);
+    const LagrangeDen<WF> L;
+    const int lo0 = __ldg(f.win + 6 * c), lo1 = __ldg(f.win + 6 * c + 1), lo2 = __ldg(f.win + 6 * c + 2);
+    const int ext0 = __ldg(f.win + 6 * c + 3), ext1 = __ldg(f.win + 6 * c + 4), ext2 = __ldg(f.win + 6 * c + 5);
+    const int wn = ext0 * ext1 * ext2;
+    const bool in_smem = wn <= f.cap;
+    cplx* dst = in_smem ? wgrid : f.slots + (int64_t)c * nf;
+    for (int t = lane; t < wn; t += 32) dst[t] = mk(0.0);
+    const int grp = lane >> 3, h = (lane & 7) >> 2, tc = lane & 3;
+    // taps this lane adds to the window at a run end: ta = grp, tb = 2 h + j
+    int od[2];
+    bool tok[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int tb = 2 * h + j;
+        tok[j] = grp < fs.w[0] && tb < fs.w[1] && tc < fs.w[2];
+        od[j] = (grp * ext1 + tb) * ext2 + tc;
+    }
+    double accr[4][2], acci[4][2];
+#pragma unroll
+    for (int ta = 0; ta < 4; ++ta)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) accr[ta][j] = acci[ta][j] = 0.0;
+    int c0 = -1, c1 = 0, c2 = 0;
+    auto flush = [&]() {
+        const int base = ((c0 - lo0) * ext1 + (c1 - lo1)) * ext2 + (c2 - lo2);
+#pragma unroll
+        for (int ta = 0; ta < 4; ++ta)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                double vr = accr[ta][j], vi = acci[ta][j];
+                vr += __shfl_xor_sync(0xffffffffu, vr, 8);
+                vi += __shfl_xor_sync(0xffffffffu, vi, 8);
+                vr += __shfl_xor_sync(0xffffffffu, vr, 16);
+                vi += __shfl_xor_sync(0xffffffffu, vi, 16);
+                if (ta == grp && tok[j]) {
+                    cplx& d = dst[base + od[j]];
+                    d.re += vr;
+                    d.im += vi;
+                }
+                accr[ta][j] = acci[ta][j] = 0.0;
+            }
+        __syncwarp();
+    };
+    __syncwarp();
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int64_t p = base + lane;
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int s0 = c0, s1 = c1, s2 = c2;
+        __syncwarp();
+        if (p < p1) {
+            double* r = stage + lane * REC;
+            s0 = fast_stencil<WF>(__ldg(f.pos + 3 * p), fs.n[0], fs.origin[0], fs.h[0], f.rf[0], L, r);
+            s1 = fast_stencil<WF>(__ldg(f.pos + 3 * p + 1), fs.n[1], fs.origin[1], fs.h[1], f.rf[1], L, r + WF);
+            s2 = fast_stencil<WF>(__ldg(f.pos + 3 * p + 2), fs.n[2], fs.origin[2], fs.h[2], f.rf[2], L, r + 2 * WF);
+            const double2 qv = __ldg(reinterpret_cast<const double2*>(f.q + p));
+            r[3 * WF] = qv.x;
+            r[3 * WF + 1] = qv.y;
+        }
+        int q0 = __shfl_up_sync(0xffffffffu, s0, 1), q1 = __shfl_up_sync(0xffffffffu, s1, 1),
+            q2 = __shfl_up_sync(0xffffffffu, s2, 1);
+        if (lane == 0) {
+            q0 = c0;
+            q1 = c1;
+            q2 = c2;
+        }
+        const unsigned heads = __ballot_sync(0xffffffffu, lane < cnt && (s0 != q0 || s1 != q1 || s2 != q2));
+        __syncwarp();
+        int j = 0;
+        while (j < cnt) {
+            if ((heads >> j) & 1u) {
+                if (c0 >= 0) flush();
+                c0 = __shfl_sync(0xffffffffu, s0, j);
+                c1 = __shfl_sync(0xffffffffu, s1, j);
+                c2 = __shfl_sync(0xffffffffu, s2, j);
+            }
+            const unsigned rest = j < 31 ? heads & (0xffffffffu << (j + 1)) : 0u;
+            const int e = rest ? __ffs(rest) - 1 : cnt;
+            for (int k = j + grp; k < e; k += 4) {
+                const double* r = stage + k * REC;
+                const double2 wx01 = *reinterpret_cast<const double2*>(r);
+                const double2 wx23 = *reinterpret_cast<const double2*>(r + 2);
+                const double2 wy = *reinterpret_cast<const double2*>(r + WF + 2 * h);
+                const double wz = r[2 * WF + tc];
+                const double2 qv = *reinterpret_cast<const double2*>(r + 3 * WF);
+                const double wx[4] = {wx01.x, wx01.y, wx23.x, wx23.y};
+#pragma unroll
+                for (int ta = 0; ta < 4; ++ta) {
+                    const double w0 = (wx[ta] * wy.x) * wz, w1 = (wx[ta] * wy.y) * wz;
+                    accr[ta][0] += w0 * qv.x;
+                    acci[ta][0] += w0 * qv.y;
+                    accr[ta][1] += w1 * qv.x;
+                    acci[ta][1] += w1 * qv.y;
+                }
+            }
+            __syncwarp();
+            j = e;
+        }
+    }
+    if (c0 >= 0) flush();
+    if (in_smem) {
+        cplx* out = f.slots + (int64_t)c * nf;
+        for (int t = lane; t < wn; t += 32) out[t] = wgrid[t];
+    }
+}
+
 // far node t: sum of the chunk windows covering it, chunks in a fixed tree order
 __global__ void __launch_bounds__(256) k_far_windows_reduce(FarWinArgs f, int nfx, int nfy, int nfz, cplx* qg) {
     const int t = blockIdx.x;
@@ -1218,47 +1356,79 @@ __global__ void __launch_bounds__(256) k_far_windows_reduce(FarWinArgs f, int nf
     if (threadIdx.x == 0) qg[t] = red[0];
 }
 
-int far_win_chunk(int64_t n) {
-    int64_t c = n / (148 * 16);
-    c = std::max<int64_t>(256, std::min<int64_t>(2048, c));
+// points per warp chunk for `slots` resident warps (one wave, equal chunks)
+static int far_chunk_for(int64_t n, int slots) {
+    int64_t c = (n + slots - 1) / slots;
+    c = std::max<int64_t>(256, std::min<int64_t>(4096, c));
     return (int)((c + 31) / 32 * 32);
 }
 
-// plan build: the chunk windows of n sorted points (read by k_far_project_win2)
-void launch_far_win_bounds(const StencilGeom& fs, const double* pos, int64_t n, int* win, cudaStream_t s) {
+// Plan build: choose the chunk length and the shared-memory window capacity, and
+// compute the chunk windows of the n sorted points.  First choice: one wave of
+// 3 blocks x 8 warps per SM with 256-entry windows (more resident warps hide the
+// dependent FP64 chains); if a chunk's window is larger, 2 blocks per SM with
+// 400-entry windows (larger windows accumulate in their global slot).
+// FFTPIM_FAR_CAP=400 forces the second choice.
+void far_win_setup(const StencilGeom& fs, const double* pos, int64_t n, int* win, int* chunk_out, int* cap_out,
+                   cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const int forced = [] {
+        const char* e = getenv("FFTPIM_FAR_CAP");
+        return e ? atoi(e) : 0;
+    }();
+    *chunk_out = far_chunk_for(n, sms * 2 * FPW_WARPS);
+    *cap_out = FPW_CAP;
     if (!pos || !win || n <= 0) return;
-    FarWinArgs f;
-    f.pos = pos;
-    f.q = nullptr;
-    f.n = n;
-    f.chunk = far_win_chunk(n);
-    f.nchunks = (int)((n + f.chunk - 1) / f.chunk);
-    f.slots = nullptr;
-    f.win = win;
-    for (int ax = 0; ax < 3; ++ax) f.rf[ax] = fs.h[ax] > 0 ? 1.0 / fs.h[ax] : 0.0;
-    const int blocks = (f.nchunks + 7) / 8;
-    switch (fs.order + 1) {
-        case 3: k_far_win_bounds<3><<<blocks, 256, 0, s>>>(fs, f); break;
-        case 4: k_far_win_bounds<4><<<blocks, 256, 0, s>>>(fs, f); break;
-        case 5: k_far_win_bounds<5><<<blocks, 256, 0, s>>>(fs, f); break;
-        default: return;
+    for (int attempt = forced == FPW_CAP ? 1 : 0; attempt < 2; ++attempt) {
+        FarWinArgs f;
+        f.pos = pos;
+        f.q = nullptr;
+        f.n = n;
+        f.chunk = far_chunk_for(n, sms * (attempt == 0 ? 3 : 2) * FPW_WARPS);
+        f.nchunks = (int)((n + f.chunk - 1) / f.chunk);
+        f.cap = attempt == 0 ? 256 : FPW_CAP;
+        f.slots = nullptr;
+        f.win = win;
+        for (int ax = 0; ax < 3; ++ax) f.rf[ax] = fs.h[ax] > 0 ? 1.0 / fs.h[ax] : 0.0;
+        const int blocks = (f.nchunks + 7) / 8;
+        switch (fs.order + 1) {
+            case 3: k_far_win_bounds<3><<<blocks, 256, 0, s>>>(fs, f); break;
+            case 4: k_far_win_bounds<4><<<blocks, 256, 0, s>>>(fs, f); break;
+            case 5: k_far_win_bounds<5><<<blocks, 256, 0, s>>>(fs, f); break;
+            default: return;
+        }
+        fftpim_count_launch();
+        *chunk_out = f.chunk;
+        *cap_out = f.cap;
+        if (attempt == 1) return;
+        std::vector<int> h((size_t)f.nchunks * 6);
+        cudaMemcpyAsync(h.data(), win, h.size() * sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        int worst = 0;
+        for (int c = 0; c < f.nchunks; ++c) worst = std::max(worst, h[6 * c + 3] * h[6 * c + 4] * h[6 * c + 5]);
+        if (worst <= f.cap) return;
     }
-    fftpim_count_launch();
 }
 
+// upper bound of the chunk count over both choices (slot allocation)
+int64_t far_win_max_chunks(int64_t n) { return (n + 255) / 256 + 1; }
+
 bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, int* win, cudaStream_t s) {
-    if (!pos || !slots) return false;
+    if (!pos || !slots || a.far_chunk <= 0) return false;
     FarWinArgs f;
     f.pos = pos;
     f.q = a.far_q;
     f.n = a.far_n;
-    f.chunk = far_win_chunk(a.far_n);
+    f.chunk = a.far_chunk;
     f.nchunks = (int)((a.far_n + f.chunk - 1) / f.chunk);
+    f.cap = a.far_cap;
     f.slots = slots;
     f.win = win;
     for (int ax = 0; ax < 3; ++ax) f.rf[ax] = a.fs.h[ax] > 0 ? 1.0 / a.fs.h[ax] : 0.0;
     const int WF = a.fs.order + 1;
-    const size_t smem = (size_t)FPW_WARPS * (FPW_CAP * sizeof(cplx) + 32 * (3 * WF + 2) * sizeof(double) +
+    const size_t smem = (size_t)FPW_WARPS * (f.cap * sizeof(cplx) + 32 * (3 * WF + 2) * sizeof(double) +
                                              32 * 3 * sizeof(int));
     const int blocks = (f.nchunks + FPW_WARPS - 1) / FPW_WARPS;
     // FFTPIM_FAR_WIN2=1: plan-time windows + ballot-split runs (k_far_project_win2).  Bit-identical, 30 %
@@ -1281,6 +1451,23 @@ bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, i
         else
             kern<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
     };
+    // FFTPIM_FAR_WIN4=0: order-3 stencils through the general kernel (one point per warp step)
+    static const bool v4 = [] {
+        const char* e = getenv("FFTPIM_FAR_WIN4");
+        return !(e && e[0] == '0');
+    }();
+    if (WF == 4 && v4 && !v2) {
+        static size_t configured4 = 48 * 1024;
+        if (smem > configured4) {
+            cudaFuncSetAttribute(k_far_project_win4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured4 = smem;
+        }
+        if (f.nchunks > 0) k_far_project_win4<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
+        const int nf4 = a.fs.n[0] * a.fs.n[1] * a.fs.n[2];
+        k_far_windows_reduce<<<nf4, 256, 0, s>>>(f, a.fs.n[0], a.fs.n[1], a.fs.n[2], a.far_qg);
+        fftpim_count_launch(2);
+        return true;
+    }
     switch (WF) {
         case 3: go(k_far_project_win<3>, k_far_project_win2<3>); break;
         case 4: go(k_far_project_win<4>, k_far_project_win2<4>); break;

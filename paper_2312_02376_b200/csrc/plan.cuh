@@ -190,6 +190,7 @@ struct FftpimPlan {
     cplx* far_partial = nullptr;  // per-block partial grids
     cplx* far_slots = nullptr;    // windowed far projection (line_kernels.cu): per-chunk windows
     int* far_win = nullptr;
+    int far_chunk = 0, far_cap = 0;
     cplx* far_ug = nullptr;       // far observer-grid potentials
     cplx* obs_pre = nullptr;      // split observer pass: far + K4 fix-up (concurrent schedule)
     int far_blocks_seq = 0;            // far projection grid for sequential chains

@@ -84,15 +84,21 @@ def test_k4_16bit_offsets_bitwise(case, tmp_path):
 
 @pytest.mark.parametrize("case", ["c2", "blobs3d", "p2_planar_npsp", "p1_axis_dyn", "p3_dyn"])
 def test_far_windows_from_the_plan_bitwise(case, tmp_path):
-    """Windowed far projection reading the plan-time chunk windows and splitting
-    staged batches into runs by ballot (k_far_project_win2) against the kernel
-    that recomputes the windows and tests every point (k_far_project_win): same
-    chunks, runs and summation order -> identical bits; both within rounding of
-    the stored-weight projection."""
+    """Windowed far projection variants.  k_far_project_win2 (plan-time chunk windows,
+    staged batches split into runs by ballot) against k_far_project_win (windows
+    recomputed, every point tested): same chunks, runs and summation order ->
+    identical bits.  k_far_project_win4 (order-3 stencils, four points per warp
+    step, group sums added in a fixed shuffle order; the default) agrees to
+    rounding and is bitwise reproducible; all within rounding of the
+    stored-weight projection."""
     u2, _ = run_variant(case, {"FFTPIM_FAR": "win", "FFTPIM_FAR_WIN2": "1"}, tmp_path, "win2")
-    u1, _ = run_variant(case, {"FFTPIM_FAR": "win"}, tmp_path, "win1")
+    u1, _ = run_variant(case, {"FFTPIM_FAR": "win", "FFTPIM_FAR_WIN4": "0"}, tmp_path, "win1")
+    u4, _ = run_variant(case, {"FFTPIM_FAR": "win"}, tmp_path, "win4")
+    u4b, _ = run_variant(case, {"FFTPIM_FAR": "win"}, tmp_path, "win4b")
     uw, _ = run_variant(case, {"FFTPIM_FAR": "warps"}, tmp_path, "warps")
     np.testing.assert_array_equal(u2, u1)
+    np.testing.assert_array_equal(u4, u4b)
+    assert rel_l2(u4, u1) <= 1e-13
     assert rel_l2(u2, uw) <= 1e-13
 
 
