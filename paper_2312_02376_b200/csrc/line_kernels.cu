@@ -1451,10 +1451,12 @@ bool launch_far_project_win(const EvalArgs& a, const double* pos, cplx* slots, i
         else
             kern<<<blocks, 32 * FPW_WARPS, smem, s>>>(a, f);
     };
-    // FFTPIM_FAR_WIN4=0: order-3 stencils through the general kernel (one point per warp step)
+    // FFTPIM_FAR_WIN4=1: order-3 stencils, four points per warp step (k_far_project_win4).  Measured 2.2x slower
+    // than the general kernel (C4 2.12 vs 0.97 ms, C5 0.55-0.62 vs 0.27 ms, C3 0.37-0.40 vs 0.16 ms): runs of equal
+    // starts are ~13 points, so the 128 shuffles of the group reduction per run outweigh the shorter point loop
     static const bool v4 = [] {
         const char* e = getenv("FFTPIM_FAR_WIN4");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     if (WF == 4 && v4 && !v2) {
         static size_t configured4 = 48 * 1024;
