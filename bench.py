@@ -341,6 +341,10 @@ def run_b200(args):
                          "far chain, split observer pass" if int(info.n_pairs) <= 500_000_000 else
                          "chains in order (K4 uses the whole chip)"),
             "stage_gbs": {k: nbytes[k] / (prof[k] * 1e-3) / 1e9 for k in nbytes if prof.get(k, 0) > 0},
+            # SURVEY.md 8d "end to end": every stage's algorithmic bytes over the whole step time
+            "roofline_whole_evaluation": {"algorithmic_bytes": int(sum(nbytes.values())),
+                                          "achieved": sum(nbytes.values()) / (ms_max * 1e-3) / 1e9, "unit": "GB/s",
+                                          "frac": sum(nbytes.values()) / (ms_max * 1e-3) / 1e9 / peak},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * w.n_points,
                     "d2h_bytes_per_step": 16 * w.n_points, "buffers": "pinned host (evaluate(q, out=u))"},
             "e2e_pageable": {"value": e2e_pageable, "unit": UNIT, "calls": n_pg,
