@@ -455,8 +455,15 @@ struct RegE {
 
 // TS: stride into the twiddle table (1: tw has L entries; 3: tw is the table
 // of a length-3L transform, w_L^m = tw[3 m])
-template <int L, int SIGN, int TS = 1, bool IP = false>
-__device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw) {
+struct RegNoOp {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// `mid` runs right after the exchange barrier, when the first-level values have
+// left the registers: the fused x stage issues its spectrum loads there, so their
+// DRAM latency overlaps the second-level DFTs
+template <int L, int SIGN, int TS = 1, bool IP = false, class Mid = RegNoOp>
+__device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t, const cplx* tw, Mid mid = Mid()) {
     constexpr int E = RegE<L>::E, T = L / E;
     if constexpr (IP)
         dft_reg_ip<E, SIGN>(a);
@@ -467,6 +474,7 @@ __device__ __forceinline__ void reg_fwd(cplx (&a)[RegE<L>::E], cplx* buf, int t,
 #pragma unroll
     for (int k1 = 0; k1 < E; ++k1) buf[k1 * (T + 1) + t] = a[k1];
     __syncthreads();
+    mid();
 #pragma unroll
     for (int s = 0; s < E / T; ++s) {
         cplx b[T];
@@ -505,6 +513,9 @@ __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t,
 }
 
 #define RF_THREADS 128
+#ifndef FFT_SPEC_EARLY   // fused x stage: spectrum loads issued before the second-level DFTs
+#define FFT_SPEC_EARLY 1
+#endif
 #ifndef FFT_PF_FOLDED   // L2 prefetch of the spectrum rows also when the table is read at folded columns
 #define FFT_PF_FOLDED 0   // measured slower at C4 (x stage 1.41 -> 1.64 ms)
 #endif
@@ -558,7 +569,6 @@ __global__ void __launch_bounds__(RF_THREADS, (L == 512 && IP) ? RF_MINB512 : 1)
     cplx* buf = xs + c * CS;
     cplx* out = st.out + (int64_t)blockIdx.y * st.out_s1 + (int64_t)col * st.out_s0;
     if (st.spec) {
-        reg_fwd<L, -1, 1, IP>(a, buf, t, st.tw);
         int64_t fcol = col;
         if (st.fold_y | st.fold_z) {
             int ky = col / st.spec_L2, kz = col - ky * st.spec_L2;
@@ -567,6 +577,22 @@ __global__ void __launch_bounds__(RF_THREADS, (L == 512 && IP) ? RF_MINB512 : 1)
             fcol = (int64_t)ky * st.spec_L2 + kz;
         }
         const cplx* sp = st.spec + (int64_t)blockIdx.y * st.spec_s1 + fcol * st.spec_s0;
+#if FFT_SPEC_EARLY
+        cplx kh[E];
+        reg_fwd<L, -1, 1, IP>(a, buf, t, st.tw, [&]() {
+            if (okc) {
+#pragma unroll
+                for (int s = 0; s < E / T; ++s)
+#pragma unroll
+                    for (int k2 = 0; k2 < T; ++k2) kh[s * T + k2] = sp[(int64_t)(t + T * s + E * k2) * st.spec_stride];
+            }
+        });
+        if (okc) {
+#pragma unroll
+            for (int j = 0; j < E; ++j) a[j] = a[j] * kh[j];
+        }
+#else
+        reg_fwd<L, -1, 1, IP>(a, buf, t, st.tw);
         if (okc) {
 #pragma unroll
             for (int s = 0; s < E / T; ++s)
@@ -574,6 +600,7 @@ __global__ void __launch_bounds__(RF_THREADS, (L == 512 && IP) ? RF_MINB512 : 1)
                 for (int k2 = 0; k2 < T; ++k2)
                     a[s * T + k2] = a[s * T + k2] * sp[(int64_t)(t + T * s + E * k2) * st.spec_stride];
         }
+#endif
         reg_inv<L, 1, IP>(a, buf, t, st.tw);
 #pragma unroll
         for (int n1 = 0; n1 < E; ++n1) {

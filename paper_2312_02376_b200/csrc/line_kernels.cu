@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(K1L_NT, K1L_MINB) k_k1_lines(EvalArgs a, const
                     rp[1] = qq[u].y;
                     fast_stencil<W>(px[u], g.n[0], g.origin[0], g.h[0], rh0, L, rp + 2);
                     fast_stencil<W>(py[u], g.n[1], g.origin[1], g.h[1], rh1, L, rp + 2 + W);
-                    rp[2 + 3 * W] = (double)fast_stencil<W>(pz[u], g.n[2], g.origin[2], g.h[2], rh2, L, rp + 2 + 2 * W);
+                    // the z start rides in the record's last slot as an int (no F2I in the point loop)
+                    *reinterpret_cast<int*>(rp + 2 + 3 * W) = fast_stencil<W>(pz[u], g.n[2], g.origin[2], g.h[2], rh2, L, rp + 2 + 2 * W);
                 }
                 __syncthreads();
                 // this thread's point ranges of the W rows it reads, flattened
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(K1L_NT, K1L_MINB) k_k1_lines(EvalArgs a, const
 #pragma unroll
                     for (int ia = 0; ia < W; ++ia) wx[ia] = rp[2 + ia];
                     const double wy = rp[2 + W + ib];
-                    const int sz = (int)rp[2 + 3 * W];
+                    const int sz = *reinterpret_cast<const int*>(rp + 2 + 3 * W);
                     const double qyr = qv.x * wy, qyi = qv.y * wy;
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
@@ -762,13 +763,23 @@ __global__ void __launch_bounds__(K3T_NT, K3T_MINB) k_observers_tile(EvalArgs a,
     // grid tile: nodes (sx0 + ex, sy0 + ey, sz0 + ez), clipped to the grid
     {
         const int m0 = g.n[0], m1 = g.n[1], m2 = g.n[2];
-        for (int e = threadIdx.x; e < T::NODES; e += K3T_NT) {
+        // all of a thread's node loads are issued before the first store (one exposed
+        // global latency per block instead of one per node)
+        constexpr int NLD = (T::NODES + K3T_NT - 1) / K3T_NT;
+        cplx v[NLD];
+#pragma unroll
+        for (int u = 0; u < NLD; ++u) {
+            const int e = threadIdx.x + u * K3T_NT;
             const int ez = e % T::EZ, ey = (e / T::EZ) % T::EY, ex = e / (T::EZ * T::EY);
             const int x = sx0 + ex, y = sy0 + ey, z = sz0 + ez;
-            cplx v = mk(0.0);
-            if (x < m0 && x < sxe + W - 1 && y < m1 && z < m2)
-                v = a.interp_grid[((int64_t)(x - a.gx0) * a.gi1 + y) * a.gi2 + z];
-            tile[e] = v;
+            v[u] = mk(0.0);
+            if (e < T::NODES && x < m0 && x < sxe + W - 1 && y < m1 && z < m2)
+                v[u] = a.interp_grid[((int64_t)(x - a.gx0) * a.gi1 + y) * a.gi2 + z];
+        }
+#pragma unroll
+        for (int u = 0; u < NLD; ++u) {
+            const int e = threadIdx.x + u * K3T_NT;
+            if (e < T::NODES) tile[e] = v[u];
         }
         if (far)
             for (int t = threadIdx.x; t < nf; t += K3T_NT) sfar[t] = a.far_ug[t];
