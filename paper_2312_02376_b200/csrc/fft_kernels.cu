@@ -514,7 +514,7 @@ __device__ __forceinline__ void reg_inv(cplx (&a)[RegE<L>::E], cplx* buf, int t,
 
 #define RF_THREADS 128
 #ifndef FFT_SPEC_EARLY   // fused x stage: spectrum loads issued before the second-level DFTs
-#define FFT_SPEC_EARLY 1
+#define FFT_SPEC_EARLY 0   // measured slower at C4 (x stage 1.55-1.57 vs 1.39-1.49 ms: 176 B of spills at 255 registers), C2 equal
 #endif
 #ifndef FFT_PF_FOLDED   // L2 prefetch of the spectrum rows also when the table is read at folded columns
 #define FFT_PF_FOLDED 0   // measured slower at C4 (x stage 1.41 -> 1.64 ms)
