@@ -97,8 +97,8 @@ def full(rep, js, label="C2", source=None):
         doc = {}
     doc[label] = traffic
     doc.setdefault("sources", {})[label] = source or rep
-    doc["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, first launch of each stage kernel "
-                   "in the --set full capture named in sources")
+    doc.setdefault("note", "dram__bytes_read.sum + dram__bytes_write.sum per launch, first launch of each stage kernel "
+                           "in the --set full capture named in sources")
     doc.pop("source", None)
     json.dump(doc, open(js, "w"), indent=1)
 

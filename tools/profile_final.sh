@@ -3,7 +3,7 @@
 # reference arm with the driver's flags, the ncu launch list of the default bench command and a --set full capture of one
 # evaluation's kernels.  Each ncu pass runs after the same command exited 0 without ncu.  Outputs: gpurun_out/final/.
 set -u
-OUT=gpurun_out/final
+OUT=${OUT:-gpurun_out/final}
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.max.sm,clocks.max.mem,power.limit --format=csv > $OUT/gpu.txt
 timeout 2400 python -m pytest tests -q -m gpu -x > $OUT/gpu_tests.log 2>&1; echo "gpu tests rc=$?"; tail -3 $OUT/gpu_tests.log
